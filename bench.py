@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark: batched windowed-DTW 1-NN search (TC-DTW cascade) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+A step is one pass of the hot path over one batch of synthetic input: every
+query of the config searched against the whole (sharded) candidate
+collection, which stays resident in HBM like a database index (it is 3 GB
+at C4, far above the 126 MB L2, so no L2 flush is needed between steps).
+
+value  = whole-job queries/s, device-timed (CUDA events), queries resident.
+e2e    = queries/s through the public API (SearchIndex.search) with pinned
+         host query buffers: H2D of the queries and D2H of (index, distance)
+         inside the timed region.
+Rank 0 prints one JSON line.  With --impl reference the CPU arm (the C port
+of the reference algorithm in oracle/, all host threads) runs instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "1-NN queries/sec (GCUPS and roofline reported alongside)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--window-index", type=int, default=0)
+    ap.add_argument("--method", default="tc_dtw")
+    ap.add_argument("--queries", type=int, default=0, help="use only the first Q queries (0 = all)")
+    ap.add_argument("--candidates", type=int, default=0, help="override N_c (0 = config)")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--seeds", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-exchange", action="store_true", help="skip the d_best all-reduce between phases")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"tcdtw_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in self.path.read_text().strip().splitlines() if r.strip()]
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(nm)
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": sorted(reasons), "samples": len(rows)}
+        try:
+            self.path.unlink()
+        except Exception:
+            pass
+        return out
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            pass
+    return {}
+
+
+# -------------------------------------------------------- CPU (oracle) legs
+def cpu_queries_per_sec(wl, w, method, advanced, n_queries_hint, budget_s, threads=0):
+    """Time the C port of the reference algorithm (oracle/, all threads) on
+    a bounded sample of the queries against the full collection."""
+    from oracle import oracle as O
+
+    cands64 = wl.candidates.astype(np.float64)
+    params = O.make_params(w, method)
+    threads = threads or (os.cpu_count() or 1)
+    # one probe query on one thread to size the sample
+    t0 = time.perf_counter()
+    O.nn_search_batch(wl.queries[:1].astype(np.float64), cands64, params, advanced, wl.dim_range, n_threads=1)
+    t1 = time.perf_counter() - t0
+    per_query = max(t1, 1e-3)
+    nq = int(max(1, min(len(wl.queries), n_queries_hint or 10 ** 9,
+                        round(budget_s / per_query * max(1, threads) * 0.8))))
+    nq = max(nq, min(threads, len(wl.queries)))
+    qs = wl.queries[1:1 + nq].astype(np.float64) if len(wl.queries) > nq else wl.queries[:nq].astype(np.float64)
+    t0 = time.perf_counter()
+    _, used = O.nn_search_batch(qs, cands64, params, advanced, wl.dim_range, n_threads=threads)
+    wall = time.perf_counter() - t0
+    return {"value": len(qs) / wall, "unit": "queries/s", "cores": int(used), "kind": "port",
+            "sample": f"{len(qs)} queries x {len(wl.candidates)} candidates, method {method}"
+                      f"{'/' + advanced if advanced else ''}, W={w}, C port of mvdtw.nn_search "
+                      f"(oracle/tcdtw_oracle.c), OpenMP over queries",
+            "wall_s": wall}
+
+
+# ----------------------------------------------------------------- main arms
+def resolve_method(P, wl, w, method, dim_range):
+    """The reference CLI's setup stage (cli.py:228-235): tune_params and,
+    for tc_dtw, tc_dtw_select on the seeded sample; untimed."""
+    params = P.SearchParams(window=w, method=P.Method(method))
+    advanced = None
+    if params.method == P.Method.TC_DTW:
+        params = P.tune_params(list(wl.queries[:64].astype(np.float64)), list(wl.candidates[:4096].astype(np.float64)),
+                               params, seed=0, dim_range=dim_range)
+        rng = np.random.default_rng(0)
+        sq = [wl.queries[i].astype(np.float64) for i in sorted(rng.choice(len(wl.queries), 8, replace=False))]
+        sc = [wl.candidates[i].astype(np.float64) for i in sorted(rng.choice(len(wl.candidates), 23, replace=False))]
+        advanced = P.tc_dtw_select(sq, sc, params, dim_range=dim_range)
+    elif params.method in (P.Method.LB_TI, P.Method.LB_PC, P.Method.LB_AD):
+        params = P.tune_params(list(wl.queries[:64].astype(np.float64)), list(wl.candidates[:4096].astype(np.float64)),
+                               params, seed=0, dim_range=dim_range)
+    return params, advanced
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2101_07731_b200.datasets import make_workload
+    import paper_2101_07731_b200.core as core
+
+    wl = make_workload(args.config, n_candidates=args.candidates or None, n_queries=args.queries or None)
+    w = wl.spec.windows()[args.window_index]
+    method, advanced = args.method, None
+    if method == "tc_dtw":
+        advanced = os.environ.get("TCDTW_REF_ADVANCED", "lb_pc")
+    del core
+    from oracle import oracle as O
+
+    cands64 = wl.candidates.astype(np.float64)
+    params = O.make_params(w, method)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    O.nn_search_batch(wl.queries[:1].astype(np.float64), cands64, params, advanced, wl.dim_range, n_threads=1)
+    per_query = time.perf_counter() - t0
+    # each step: one query per thread (bounded sample), so the run stays short
+    nq = max(1, min(len(wl.queries), threads))
+    times = []
+    for s in range(args.warmup + args.steps):
+        sel = (np.arange(nq) + s * nq) % len(wl.queries)
+        qs = wl.queries[sel].astype(np.float64)
+        t0 = time.perf_counter()
+        O.nn_search_batch(qs, cands64, params, advanced, wl.dim_range, n_threads=threads)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    step = statistics.median(times)
+    value = nq / step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8d)",
+        "config": {"workload": args.config, "n_candidates": len(wl.candidates), "n_queries_per_step": nq,
+                   "window": w, "method": method, "advanced": advanced},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "port",
+                         "sample": f"{nq} queries/step x {len(wl.candidates)} candidates (C port of "
+                                   f"mvdtw.nn_search, oracle/; single-query probe {per_query:.2f}s)"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_2101_07731_b200 as P
+    from paper_2101_07731_b200 import _lib
+    from paper_2101_07731_b200.datasets import make_workload
+    from paper_2101_07731_b200.distributed import combine_results, exchange_dbest, shard_bounds
+
+    t_gen = time.perf_counter()
+    wl = make_workload(args.config, n_candidates=args.candidates or None, n_queries=args.queries or None)
+    t_gen = time.perf_counter() - t_gen
+    w = wl.spec.windows()[args.window_index]
+    n_total = len(wl.candidates)
+    a, b = shard_bounds(n_total, world, rank)
+    params, advanced = resolve_method(P, wl, w, args.method, wl.dim_range)
+    t_up = time.perf_counter()
+    index = P.SearchIndex(wl.candidates[a:b], dtype=wl.dtype, base=a)
+    torch.cuda.synchronize()
+    t_up = time.perf_counter() - t_up
+    Qdev = index.prepare_queries(wl.queries)
+    n_q = Qdev.shape[0]
+    batch = args.batch or index.auto_batch(params, advanced, n_q, seeds=args.seeds)
+    group = None
+    hook = None
+    if world > 1 and not args.no_exchange:
+        hook = lambda d: exchange_dbest(d, group)  # noqa: E731
+
+    def step(queries, to_host=False):
+        res = index.search(queries, params, advanced=advanced, dim_range=wl.dim_range, batch=batch,
+                           seeds=args.seeds, dbest_hook=hook, return_device=True)
+        idx, dist_ = res.best_index, res.best_distance
+        if world > 1:
+            idx, dist_ = combine_results(idx, dist_, group)
+        if to_host:
+            idx, dist_ = idx.cpu(), dist_.cpu()
+        return idx, dist_, res
+
+    def timed(fn, k):
+        times = []
+        for _ in range(k):
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            if world > 1:
+                t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                ms = float(t.item())
+            times.append(ms)
+        return times
+
+    L = _lib.load_library()
+    for _ in range(args.warmup):
+        step(Qdev)
+    torch.cuda.synchronize()
+    launches0 = L.tcdtw_launch_count() if hasattr(L, "tcdtw_launch_count") else 0
+    with ClockSampler(local) as clk:
+        times = timed(lambda: step(Qdev), args.steps)
+    launches = (L.tcdtw_launch_count() - launches0) if hasattr(L, "tcdtw_launch_count") else None
+    clocks = clk.summary()
+    ms_step = statistics.median(times)
+    value = n_q / (ms_step / 1e3)
+
+    # end to end through the public API: pinned host queries in, host results out
+    Qhost = torch.from_numpy(np.ascontiguousarray(wl.queries)).pin_memory()
+    e2e_times = timed(lambda: step(Qhost, to_host=True), max(1, min(3, args.steps)))
+    e2e_ms = statistics.median(e2e_times)
+
+    # instrumented pass: phase times (CUDA events per phase), counters
+    res = index.search(Qdev, params, advanced=advanced, dim_range=wl.dim_range, batch=batch, seeds=args.seeds,
+                       timing=True, dbest_hook=hook, return_device=True)
+    ph = res.phase_ms
+    ctr = {k: v.sum().item() for k, v in res.counters.items()}
+    if world > 1:
+        vec = torch.tensor([ctr[k] for k in _lib.COUNTERS], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(vec)
+        ctr = dict(zip(_lib.COUNTERS, vec.tolist()))
+        pv = torch.tensor([ph[k] for k in _lib.PHASES], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(pv, op=torch.distributed.ReduceOp.MAX)
+        ph = dict(zip(_lib.PHASES, pv.tolist()))
+
+    # ALU issue-rate probe (FP32 FFMA, independent chains) on this box
+    sink = torch.empty(1, device="cuda")
+    lane_ops = __import__("ctypes").c_double()
+    L.tcdtw_alu_probe(0, 148 * 8, 2000, sink.data_ptr(), __import__("ctypes").byref(lane_ops),
+                      _lib.stream_ptr())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    L.tcdtw_alu_probe(0, 148 * 8, 2000, sink.data_ptr(), __import__("ctypes").byref(lane_ops),
+                      _lib.stream_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    alu_peak = lane_ops.value / (e0.elapsed_time(e1) / 1e3) / 1e12  # T lane-op/s
+
+    n, d = wl.spec.length, wl.spec.dims
+    shard_n = b - a
+    lbmv_ops = float(n_q) * shard_n * n * (5 * d + 2)  # L(5d+2) per pair
+    lbmv_bytes = (shard_n + 3 * n_q) * n * d * (4 if wl.dtype == "f32" else 8)
+    dtw_cells = ctr["dtw_cells"]
+    dtw_ms = ph["dtw"] + ph["seeds_dtw"]
+    gcups = dtw_cells / (dtw_ms / 1e3) / 1e9 if dtw_ms > 0 else None
+    dom = max(ph, key=ph.get)
+    if dom == "lb_mv":
+        achieved = lbmv_ops / (ph["lb_mv"] / 1e3) / 1e12
+        roof = {"kernel": "lbmv_matrix_kernel", "bound": "alu", "achieved": achieved, "peak": alu_peak,
+                "unit": "Tlane-op/s", "frac": achieved / alu_peak,
+                "traffic": None, "algorithmic_ops_per_launch_set": lbmv_ops,
+                "hbm_view": {"unique_bytes": lbmv_bytes,
+                             "achieved_gbs": lbmv_bytes / (ph["lb_mv"] / 1e3) / 1e9,
+                             "peak_gbs": measured_peaks().get("hbm_gbs")}}
+    else:
+        ops = dtw_cells * (2 * d + 4)
+        achieved = ops / (dtw_ms / 1e3) / 1e12
+        roof = {"kernel": "dtw_tpp_kernel", "bound": "alu", "achieved": achieved, "peak": alu_peak,
+                "unit": "Tlane-op/s", "frac": achieved / alu_peak, "traffic": None}
+    roof["peak_source"] = ("tcdtw_alu_probe FFMA issue rate measured in this run (nominal 148 SM x 128 lanes x "
+                           f"{measured_peaks().get('sm_max_mhz', 1965)} MHz = "
+                           f"{148 * 128 * measured_peaks().get('sm_max_mhz', 1965) / 1e6:.1f} T)")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        adv_name = None if advanced is None else advanced.value
+        cpu = cpu_queries_per_sec(wl, w, params.method.value, adv_name, 0, args.cpu_seconds)
+
+    if rank == 0:
+        q_bytes = Qhost.numel() * Qhost.element_size()
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (seeded generator, SURVEY 8d; UCR absent)",
+            "config": {"workload": args.config, "n_candidates": n_total, "n_queries": n_q, "length": n, "dims": d,
+                       "window": w, "method": params.method.value,
+                       "advanced": None if advanced is None else advanced.value,
+                       "trigger_ti": params.trigger_ti, "trigger_pc": params.trigger_pc,
+                       "quant_levels": params.quant_levels, "query_batch": batch,
+                       "parallelism": f"candidate shards x{world}",
+                       "l2": "inputs larger than L2 (collection resident in HBM, no flush)"},
+            "e2e": {"value": n_q / (e2e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": q_bytes,
+                    "d2h_bytes_per_step": n_q * 16},
+            "gpu_launches": launches,
+            "gcups": gcups, "dtw_cells": dtw_cells,
+            "counters": {k: ctr[k] for k in _lib.COUNTERS},
+            "phase_ms": ph,
+            "roofline": roof,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "setup_s": {"generate": t_gen, "upload": t_up},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

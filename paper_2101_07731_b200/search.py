@@ -1,0 +1,393 @@
+"""Bounded DTW 1-NN search (search.py:1-272), batched on the GPU.
+
+``nn_search`` keeps the reference's signature and returns its NnOutcome;
+``SearchIndex`` is the batched entry point: the candidate collection stays
+resident in HBM and queries are searched in batches through the C ABI
+(tcdtw_search_seed / tcdtw_search_finish).  Answers equal the reference's
+linear-scan argmin with the lowest index winning ties; the counters describe
+the GPU's own (order-free) cascade and may differ from the reference's.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _dev, _lib
+from .core import METHOD_CODE, InvalidInputError, Method, SearchParams, as_series
+
+TUNE_CANDIDATE_SAMPLE = 23
+TUNE_QUERY_SAMPLE = 8
+
+
+@dataclass
+class NnOutcome:
+    """Result and instrumentation of one query's search (search.py:37-56)."""
+
+    best_index: int
+    best_distance: float
+    dtw_computed: int = 0
+    dtw_skipped: int = 0
+    lb_mv_evals: int = 0
+    advanced_lb_evals: int = 0
+    abandon_count: int = 0
+    lb_time: float = 0.0
+    dtw_time: float = 0.0
+    total_time: float = 0.0
+    work: float = 0.0
+
+
+@dataclass
+class BatchOutcome:
+    """Per-query results of a batched search (numpy arrays)."""
+
+    best_index: np.ndarray
+    best_distance: np.ndarray
+    counters: dict
+    phase_ms: dict = field(default_factory=dict)
+    total_ms: float = 0.0
+
+    def outcome(self, i: int, work: float = 0.0) -> NnOutcome:
+        c = self.counters
+        return NnOutcome(int(self.best_index[i]), float(self.best_distance[i]), int(c["dtw_computed"][i]),
+                         int(c["dtw_skipped"][i]), int(c["lb_mv_evals"][i]), int(c["advanced_lb_evals"][i]),
+                         int(c["abandon_count"][i]), work=work)
+
+
+def _advanced_method(params: SearchParams, advanced) -> Method | None:
+    """search.py:59-68."""
+    method = params.method
+    if method in (Method.NONE, Method.LB_MV):
+        return None
+    if method == Method.TC_DTW:
+        if advanced not in (Method.LB_TI, Method.LB_PC):
+            raise InvalidInputError("TC_DTW must be resolved with tc_dtw_select first")
+        return Method(advanced)
+    return method
+
+
+def work_model(params: SearchParams, n: int, dims: int, adv: Method | None, counters: dict, i: int) -> float:
+    """The reference's deterministic work model (search.py:102-125), fed
+    with this search's own counters."""
+    w = params.effective_window(n)
+    work = 0.0
+    if params.method != Method.NONE:
+        work += n * dims
+    if adv == Method.LB_TI:
+        work += n * dims
+    elif adv == Method.LB_PC:
+        work += n * dims * (1 + params.quant_levels)
+    work += counters["lb_mv_evals"][i] * (n * dims)
+    per_adv = {Method.LB_TI: n * (4.0 + (2.0 + w / params.refresh_period) * dims),
+               Method.LB_PC: n * params.max_boxes * dims,
+               Method.LB_AD: n * (2.0 * w + 1.0) * dims}
+    if adv is not None:
+        work += counters["advanced_lb_evals"][i] * per_adv[adv]
+    work += counters["dtw_cells"][i] * dims
+    return float(work)
+
+
+def _stack(candidates) -> np.ndarray:
+    try:
+        import torch
+
+        if isinstance(candidates, torch.Tensor):
+            return candidates
+    except ImportError:  # pragma: no cover
+        pass
+    if isinstance(candidates, np.ndarray) and candidates.ndim == 3:
+        if not np.all(np.isfinite(candidates)):
+            raise InvalidInputError("series contains non-finite values")
+        return candidates
+    cas = [as_series(c) for c in candidates]
+    if not cas:
+        raise InvalidInputError("candidate list is empty")
+    shape = cas[0].shape
+    for c in cas:
+        if c.shape != shape:
+            raise InvalidInputError(f"shape mismatch: {c.shape} vs {shape}")
+    return np.stack(cas)
+
+
+class SearchIndex:
+    """A candidate collection (or one shard of it) resident on the GPU.
+
+    dtype "f64" runs the EXACT float64 path; "f32" stores float32 and runs
+    the float32 filter with float64 finalist re-scoring.  `base` is the
+    global index of candidate 0 (sharding).
+    """
+
+    def __init__(self, candidates, dtype=None, base: int = 0, device=None):
+        t = _dev.torch()
+        arr = _stack(candidates)
+        if dtype is None:
+            dtype = "f32" if getattr(arr, "dtype", None) in (np.float32, t.float32) else "f64"
+        self.dtype = "f32" if _lib.dtype_code(dtype) == _lib.F32 else "f64"
+        self.tdtype = t.float32 if self.dtype == "f32" else t.float64
+        if isinstance(arr, t.Tensor):
+            dev = arr.to(device=device or "cuda", dtype=self.tdtype).contiguous()
+        else:
+            if arr.ndim != 3 or arr.shape[0] < 1:
+                raise InvalidInputError("candidate list is empty")
+            dev = t.from_numpy(np.ascontiguousarray(arr)).to(device=device or "cuda", dtype=self.tdtype)
+        if dev.ndim != 3 or dev.shape[0] < 1:
+            raise InvalidInputError("candidate list is empty")
+        self.candidates = dev.contiguous()
+        self.base = int(base)
+        self._ws = None
+        self._ws_bytes = 0
+
+    @property
+    def n_candidates(self) -> int:
+        return int(self.candidates.shape[0])
+
+    def _desc(self, params: SearchParams, adv: Method | None, n_q: int, seeds: int, timing: bool,
+              phase_buf) -> _lib.SearchDesc:
+        _, n, d = self.candidates.shape
+        return _lib.SearchDesc(
+            dtype=_lib.dtype_code(self.dtype), n=n, dims=d, window=int(params.window),
+            method=METHOD_CODE[params.method],
+            advanced=METHOD_CODE[adv] if (params.method == Method.TC_DTW and adv is not None) else 0,
+            refresh_period=params.refresh_period, quant_levels=params.quant_levels,
+            max_boxes=params.max_boxes, group_width=params.group_width, trigger_ti=params.trigger_ti,
+            trigger_pc=params.trigger_pc, min_cell_frac=params.min_cell_frac, n_queries=n_q,
+            n_candidates=self.n_candidates, candidate_base=self.base, seeds=seeds,
+            flags=_lib.FLAG_TIMING if timing else 0,
+            phase_ms=ctypes.cast(phase_buf, ctypes.POINTER(ctypes.c_float)) if timing else None)
+
+    def workspace_bytes(self, params: SearchParams, advanced=None, n_q: int = 1, seeds: int = 0) -> int:
+        adv = _advanced_method(params, advanced)
+        desc = self._desc(params, adv, n_q, seeds, False, None)
+        out = ctypes.c_size_t()
+        _lib.check(_lib.load_library().tcdtw_search_workspace_size(ctypes.byref(desc), ctypes.byref(out)),
+                   "workspace_size")
+        return int(out.value)
+
+    def auto_batch(self, params: SearchParams, advanced=None, n_q: int = 1, budget_bytes: int | None = None,
+                   seeds: int = 0) -> int:
+        """Largest query batch whose workspace fits the budget (default:
+        half of the free device memory)."""
+        t = _dev.torch()
+        if budget_bytes is None:
+            free, _ = t.cuda.mem_get_info()
+            budget_bytes = int(free * 0.5)
+        lo, hi = 1, max(1, int(n_q))
+        if self.workspace_bytes(params, advanced, hi, seeds) <= budget_bytes:
+            return hi
+        while lo < hi:
+            mid = (lo + hi + 1) // 2
+            if self.workspace_bytes(params, advanced, mid, seeds) <= budget_bytes:
+                lo = mid
+            else:
+                hi = mid - 1
+        return lo
+
+    def _workspace(self, nbytes: int):
+        t = _dev.torch()
+        if self._ws is None or self._ws_bytes < nbytes:
+            self._ws = None
+            self._ws = t.empty(nbytes, dtype=t.uint8, device=self.candidates.device)
+            self._ws_bytes = nbytes
+        return self._ws
+
+    def release(self):
+        self._ws = None
+        self._ws_bytes = 0
+
+    def prepare_queries(self, queries):
+        t = _dev.torch()
+        Q = queries if isinstance(queries, t.Tensor) else t.from_numpy(np.ascontiguousarray(
+            np.asarray(queries, dtype=np.float32 if self.dtype == "f32" else np.float64)))
+        if Q.ndim == 2:
+            Q = Q[None]
+        Q = Q.to(device=self.candidates.device, dtype=self.tdtype).contiguous()
+        if Q.ndim != 3 or Q.shape[1:] != self.candidates.shape[1:]:
+            raise InvalidInputError(f"shape mismatch: {tuple(Q.shape[1:])} vs {tuple(self.candidates.shape[1:])}")
+        if not bool(t.isfinite(Q).all()):
+            raise InvalidInputError("series contains non-finite values")
+        return Q
+
+    def seed_phase(self, qp, params: SearchParams, advanced=None, dim_range=None, seeds: int = 0,
+                   timing: bool = False) -> dict:
+        """Phase 1 (tcdtw_search_seed) for one query batch already on the
+        device; returns the state whose ``dbest`` a sharded caller may
+        min-reduce before ``finish_phase``."""
+        t = _dev.torch()
+        adv = _advanced_method(params, advanced)
+        phase_buf = (ctypes.c_float * len(_lib.PHASES))()
+        desc = self._desc(params, adv, int(qp.shape[0]), seeds, timing, phase_buf)
+        nbytes = ctypes.c_size_t()
+        L = _lib.lib()
+        _lib.check(L.tcdtw_search_workspace_size(ctypes.byref(desc), ctypes.byref(nbytes)), "workspace_size")
+        ws = self._workspace(int(nbytes.value))
+        dr = None
+        if dim_range is not None:
+            dr = _dev.to_dev(np.asarray(dim_range, dtype=np.float64).reshape(-1), self.tdtype)
+        dbest = t.empty(int(qp.shape[0]), dtype=self.tdtype, device=qp.device)
+        _lib.check(L.tcdtw_search_seed(ctypes.byref(desc), qp.data_ptr(), self.candidates.data_ptr(), _lib.ptr(dr),
+                                       ws.data_ptr(), ws.numel(), dbest.data_ptr(), _lib.stream_ptr()),
+                   "search_seed")
+        return {"desc": desc, "ws": ws, "qp": qp, "dr": dr, "dbest": dbest, "phase_buf": phase_buf,
+                "seed_ms": list(phase_buf[:4]) if timing else None}
+
+    def finish_phase(self, state: dict, out_idx=None, out_dist=None, out_ctr=None):
+        """Phase 2 (tcdtw_search_finish); returns device tensors
+        (best_index, best_distance, counters)."""
+        t = _dev.torch()
+        qp = state["qp"]
+        nq = int(qp.shape[0])
+        if out_idx is None:
+            out_idx = t.empty(nq, dtype=t.int64, device=qp.device)
+        if out_dist is None:
+            out_dist = t.empty(nq, dtype=t.float64, device=qp.device)
+        if out_ctr is None:
+            out_ctr = t.empty((nq, len(_lib.COUNTERS)), dtype=t.int64, device=qp.device)
+        ws = state["ws"]
+        _lib.check(_lib.lib().tcdtw_search_finish(
+            ctypes.byref(state["desc"]), qp.data_ptr(), self.candidates.data_ptr(), _lib.ptr(state["dr"]),
+            ws.data_ptr(), ws.numel(), state["dbest"].data_ptr(), out_idx.data_ptr(), out_dist.data_ptr(),
+            out_ctr.data_ptr(), _lib.stream_ptr()), "search_finish")
+        return out_idx, out_dist, out_ctr
+
+    def search(self, queries, params: SearchParams, advanced=None, dim_range=None, batch: int | None = None,
+               seeds: int = 0, timing: bool = False, dbest_hook=None, return_device: bool = False) -> BatchOutcome:
+        """1-NN of every query.  `dbest_hook(d_best_tensor)` (optional) may
+        tighten the per-query best-so-far between the two phases, e.g. an
+        NCCL min-allreduce across shards.  With return_device=True the
+        result arrays stay on the GPU (torch tensors)."""
+        t = _dev.torch()
+        _advanced_method(params, advanced)
+        Q = self.prepare_queries(queries)
+        n_q = Q.shape[0]
+        if batch is None:
+            batch = self.auto_batch(params, advanced, n_q, seeds=seeds)
+        batch = max(1, min(int(batch), n_q))
+        best_idx = t.empty(n_q, dtype=t.int64, device=Q.device)
+        best_dist = t.empty(n_q, dtype=t.float64, device=Q.device)
+        counters = t.empty((n_q, len(_lib.COUNTERS)), dtype=t.int64, device=Q.device)
+        phase_tot = np.zeros(len(_lib.PHASES))
+        t_start = time.perf_counter()
+        for q0 in range(0, n_q, batch):
+            q1 = min(n_q, q0 + batch)
+            st = self.seed_phase(Q[q0:q1], params, advanced, dim_range, seeds, timing)
+            if timing:
+                phase_tot[:4] += np.array(st["seed_ms"])
+            if dbest_hook is not None:
+                dbest_hook(st["dbest"])
+            self.finish_phase(st, best_idx[q0:q1], best_dist[q0:q1], counters[q0:q1])
+            if timing:
+                phase_tot[4:] += np.array(st["phase_buf"][4:])
+        phases = dict(zip(_lib.PHASES, phase_tot.tolist()))
+        if return_device:
+            ctr = {k: counters[:, i] for i, k in enumerate(_lib.COUNTERS)}
+            return BatchOutcome(best_idx, best_dist, ctr, phases, (time.perf_counter() - t_start) * 1e3)
+        ci = counters.cpu().numpy()
+        ctr = {k: ci[:, i] for i, k in enumerate(_lib.COUNTERS)}
+        return BatchOutcome(best_idx.cpu().numpy(), best_dist.cpu().numpy(), ctr, phases,
+                            (time.perf_counter() - t_start) * 1e3)
+
+
+def nn_search_batch(queries, candidates, params: SearchParams, advanced: Method | None = None,
+                    dim_range=None, dtype=None, batch: int | None = None, timing: bool = False) -> BatchOutcome:
+    """Batched nn_search: every query against one collection."""
+    index = SearchIndex(candidates, dtype=dtype)
+    return index.search(queries, params, advanced=advanced, dim_range=dim_range, batch=batch, timing=timing)
+
+
+def nn_search(query, candidates, params: SearchParams, advanced: Method | None = None,
+              dim_range: np.ndarray | None = None) -> NnOutcome:
+    """Nearest candidate of `query` under banded DTW (search.py:75-180),
+    float64 on the GPU."""
+    t0 = time.perf_counter()
+    qa = as_series(query)
+    arr = _stack(candidates)
+    if arr.shape[0] < 1:
+        raise InvalidInputError("candidate list is empty")
+    if tuple(arr.shape[1:]) != qa.shape:
+        raise InvalidInputError(f"shape mismatch: {qa.shape} vs {tuple(arr.shape[1:])}")
+    adv = _advanced_method(params, advanced)
+    res = SearchIndex(np.asarray(arr, dtype=np.float64), dtype="f64").search(
+        qa[None], params, advanced=advanced, dim_range=dim_range, timing=True)
+    n, dims = qa.shape
+    out = res.outcome(0, work=work_model(params, n, dims, adv, res.counters, 0))
+    ph = res.phase_ms
+    out.dtw_time = (ph.get("seeds_dtw", 0.0) + ph.get("dtw", 0.0) + ph.get("finalize", 0.0)) / 1e3
+    out.lb_time = (ph.get("prep", 0.0) + ph.get("lb_mv", 0.0) + ph.get("seeds_topk", 0.0)
+                   + ph.get("compact", 0.0) + ph.get("advanced", 0.0)) / 1e3
+    out.total_time = max(time.perf_counter() - t0, out.lb_time + out.dtw_time)
+    return out
+
+
+def _sample(items: list, size: int, rng: np.random.Generator) -> list:
+    """search.py:183-187 (same draw, so tuning samples match the reference)."""
+    if len(items) <= size:
+        return list(items)
+    idx = rng.choice(len(items), size=size, replace=False)
+    return [items[i] for i in sorted(idx)]
+
+
+def _run_sample(queries, candidates, params, advanced, dim_range, metric) -> float:
+    """search.py:190-195, one batched GPU search over the sample."""
+    if not queries:
+        return 0.0
+    adv = _advanced_method(params, advanced)
+    qarr = np.stack([as_series(q) for q in queries])
+    res = SearchIndex(np.asarray(_stack(candidates), dtype=np.float64), dtype="f64").search(
+        qarr, params, advanced=advanced, dim_range=dim_range, timing=(metric == "time"))
+    n, dims = qarr.shape[1:]
+    if metric == "time":
+        return float(sum(res.phase_ms.values())) / 1e3
+    return float(sum(work_model(params, n, dims, adv, res.counters, i) for i in range(len(queries))))
+
+
+def tc_dtw_select(sample_queries, sample_candidates, params: SearchParams, dim_range=None,
+                  metric: str = "work") -> Method:
+    """Pick the cheaper of LB_TI and LB_PC on a sample (search.py:198-217);
+    ties go to LB_PC.  Costs come from the GPU search's own counters."""
+    if not sample_queries or not sample_candidates:
+        raise InvalidInputError("selection sample is empty")
+    cost_ti = _run_sample(sample_queries, sample_candidates, replace(params, method=Method.LB_TI), None, dim_range,
+                          metric)
+    cost_pc = _run_sample(sample_queries, sample_candidates, replace(params, method=Method.LB_PC), None, dim_range,
+                          metric)
+    return Method.LB_TI if cost_ti < cost_pc else Method.LB_PC
+
+
+def tune_params(queries, candidates, params: SearchParams, grids: dict | None = None, seed: int = 0,
+                dim_range=None, metric: str = "work", log: list | None = None) -> SearchParams:
+    """Grid-search trigger thresholds and quantisation level on a seeded
+    sample (search.py:220-272); same grid sizes and sampling."""
+    from .core import default_grids
+
+    grids = grids or default_grids()
+    method = params.method
+    if method in (Method.NONE, Method.LB_MV):
+        return params
+    rng = np.random.default_rng(seed)
+    sq = _sample(list(queries), TUNE_QUERY_SAMPLE, rng)
+    sc = _sample(list(candidates), TUNE_CANDIDATE_SAMPLE, rng)
+
+    def eval_grid(adv: Method, variants: list[SearchParams]) -> SearchParams:
+        best, best_cost = None, None
+        for p in variants:
+            cost = _run_sample(sq, sc, replace(p, method=adv), None, dim_range, metric)
+            if log is not None:
+                log.append((adv, p, cost))
+            if best_cost is None or cost < best_cost:
+                best, best_cost = p, cost
+        return best
+
+    tuned = params
+    if method in (Method.LB_TI, Method.LB_AD, Method.TC_DTW):
+        adv = Method.LB_TI if method == Method.TC_DTW else method
+        cands = [replace(params, trigger_ti=e) for e in grids["trigger_ti"]]
+        tuned = replace(tuned, trigger_ti=eval_grid(adv, cands).trigger_ti)
+    if method in (Method.LB_PC, Method.TC_DTW):
+        cands = [replace(params, trigger_pc=e, quant_levels=lv) for e in grids["trigger_pc"]
+                 for lv in grids["quant_levels"]]
+        best = eval_grid(Method.LB_PC, cands)
+        tuned = replace(tuned, trigger_pc=best.trigger_pc, quant_levels=best.quant_levels)
+    return tuned

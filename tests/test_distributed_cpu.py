@@ -1,0 +1,73 @@
+"""World-size-2 gloo tests of the sharded-search collectives (CPU tensors).
+
+The NCCL path on the GPUs runs the same functions; here each rank holds a
+fake per-shard result and the lexicographic (distance, index) combination,
+the d_best exchange and the counter sum are checked against a host merge."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2101_07731_b200.distributed import combine_results, exchange_dbest, shard_bounds, sum_counters
+
+        rng = np.random.default_rng(7)
+        n_q = 64
+        # per-rank shard results: distances with deliberate cross-rank ties
+        dists = np.round(rng.uniform(0, 4, (world, n_q)), 1)
+        dists[:, ::7] = 1.5  # every rank ties on these queries
+        idx = np.stack([rng.integers(shard_bounds(1000, world, r)[0], shard_bounds(1000, world, r)[1], n_q)
+                        for r in range(world)])
+        idx[1, ::5] = -1  # rank 1 has no local result here
+        dists[1, ::5] = np.inf
+        my_idx = torch.tensor(idx[rank], dtype=torch.int64)
+        my_d = torch.tensor(dists[rank], dtype=torch.float64)
+        gi, gd = combine_results(my_idx, my_d)
+        # host merge: lexicographic (distance, index) over ranks
+        exp_d = dists.min(axis=0)
+        exp_i = np.array([min(idx[r, k] for r in range(world) if dists[r, k] == exp_d[k] and idx[r, k] >= 0)
+                          for k in range(n_q)])
+        ok = bool(np.array_equal(gd.numpy(), exp_d) and np.array_equal(gi.numpy(), exp_i))
+        db = torch.tensor(dists[rank], dtype=torch.float32)
+        exchange_dbest(db)
+        ok &= bool(np.array_equal(db.numpy(), dists.min(axis=0).astype(np.float32)))
+        c = torch.full((n_q, 8), rank + 1, dtype=torch.int64)
+        sum_counters(c)
+        ok &= bool((c == sum(range(1, world + 1))).all())
+        q.put((rank, ok))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("world", [2])
+def test_combine_and_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(v is True for v in results.values()), results

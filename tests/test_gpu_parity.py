@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors and the pinned C oracle.
+
+Tolerances: float64 paths are compared bit-for-bit (==), which is stricter
+than the north star's 1e-9 relative; float32 configs must return identical
+indices and distances within 1e-4 relative of the oracle (float64 on the
+float32-rounded inputs) -- the float64 finalist re-score makes them exact in
+practice, and the tests assert <= 1e-12 where that holds.
+"""
+
+import numpy as np
+import pytest
+
+from golden_io import dr_or_none, load_cases, thr_or_none
+
+pytestmark = pytest.mark.gpu
+
+TI_NAMES = ["basic", "top", "tip", "tip_top"]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2101_07731_b200 as pkg
+
+    return pkg
+
+
+# ------------------------------------------------------------ per-pair API
+def test_dtw_banded_golden(P):
+    for case in load_cases("dtw"):
+        j = 0
+        while f"dist{j}" in case:
+            r = P.dtw_banded(case["q"], case["c"], case["w"], thr_or_none(case[f"thr{j}"]))
+            assert r.distance == case[f"dist{j}"]
+            assert r.abandoned == case[f"ab{j}"]
+            assert r.cells == case[f"cells{j}"]
+            j += 1
+
+
+def test_dtw_pairs_batched_matches_single(P, rng):
+    from oracle import oracle as O
+
+    for n, d, w in ((17, 3, 4), (64, 8, 10), (40, 20, 3), (9, 1, 0)):
+        A = np.cumsum(rng.normal(size=(50, n, d)), axis=1)
+        B = np.cumsum(rng.normal(size=(50, n, d)), axis=1)
+        dist, ab, cells = P.dtw_banded_pairs(A, B, w)
+        for p in range(50):
+            od, oab, oc = O.dtw_banded(A[p], B[p], w)
+            assert dist[p] == od and ab[p] == oab and cells[p] == oc
+
+
+def test_point_distance(P, rng):
+    for _ in range(20):
+        a, b = rng.normal(size=5), rng.normal(size=5)
+        assert P.point_distance(a, b) == float(np.sqrt(((a - b) ** 2).sum()))
+
+
+def test_envelope_golden(P):
+    for case in load_cases("envelope"):
+        env = P.build_envelope(case["q"], case["w"])
+        assert np.array_equal(env.upper, case["upper"]) and np.array_equal(env.lower, case["lower"])
+        assert env.window == case["weff"]
+
+
+def test_lb_mv_lb_ad_steps_golden(P):
+    for case in load_cases("lb_mv_ad"):
+        env = P.build_envelope(case["q"], case["w"])
+        for j in range(3):
+            r = P.lb_mv(case["c"], env, thr_or_none(case[f"mv_thr{j}"]))
+            assert r.value == case[f"mv{j}"] and r.abandoned == case[f"mv_ab{j}"]
+            r = P.lb_ad(case["q"], case["c"], case["w"], thr_or_none(case[f"ad_thr{j}"]))
+            assert r.value == case[f"ad{j}"] and r.abandoned == case[f"ad_ab{j}"]
+        if len(case["q"]) > 1:
+            assert np.array_equal(P.neighbor_steps(case["q"]), case["steps_q"])
+
+
+def test_ti_advance_golden(P):
+    from paper_2101_07731_b200.lb_ti import ti_advance_batch
+
+    adv = load_cases("lb_ti")[0]["adv"]
+    lo, up = ti_advance_batch(adv[:, 0], adv[:, 1], adv[:, 2])
+    assert np.array_equal(lo.cpu().numpy(), adv[:, 3]) and np.array_equal(up.cpu().numpy(), adv[:, 4])
+    assert P.ti_advance(2.5, 4.0, 0.0) == (2.5, 4.0)
+    assert P.ti_extend_top(3.0, 6.0, 0.0) == (3.0, 6.0)
+
+
+def test_lb_ti_golden(P):
+    for case in load_cases("lb_ti")[1:]:
+        for k in range(case["nv"]):
+            r = P.lb_ti(case["q"], case["c"], case["w"], TI_NAMES[case[f"v{k}_variant"]], case[f"v{k}_period"],
+                        abandon_above=thr_or_none(case[f"v{k}_thr"]))
+            assert r.value == case[f"v{k}_val"] and r.abandoned == case[f"v{k}_ab"]
+
+
+def test_lb_ti_neighbor_reuse(P, rng):
+    q = np.cumsum(rng.normal(size=(18, 3)), axis=0)
+    c = np.cumsum(rng.normal(size=(18, 3)), axis=0)
+    nd = P.NeighborDistances.build(q, c, P.TiVariant.BASIC)
+    assert nd.candidate_steps is not None
+    assert P.lb_ti(q, c, 4, P.TiVariant.BASIC).value == P.lb_ti(q, c, 4, P.TiVariant.BASIC, neighbor=nd).value
+
+
+def test_quantize_cluster_golden(P):
+    for case in load_cases("quantize"):
+        bs = P.quantize_cluster(case["pts"], case["levels"], case["cap"], case["mcf"], dr_or_none(case["dr"]))
+        assert np.array_equal(bs.los, case["los"]) and np.array_equal(bs.his, case["his"])
+
+
+def test_box_sets_and_lb_pc_golden(P):
+    for case in load_cases("box_sets"):
+        g = P.build_box_sets(case["q"], case["w"], case["gw"], case["levels"], case["cap"], 1e-5,
+                             dr_or_none(case["dr"]))
+        assert np.array_equal(g.pad_lo, case["pad_lo"]) and np.array_equal(g.pad_hi, case["pad_hi"])
+        assert np.array_equal(g.box_counts, case["counts"])
+        assert [list(s) for s in g.spans] == case["spans"].tolist()
+        for j in range(3):
+            r = P.lb_pc(case["c"], g, thr_or_none(case[f"thr{j}"]))
+            assert r.value == case[f"val{j}"] and r.abandoned == case[f"ab{j}"]
+
+
+# ------------------------------------------------------------------ search
+RUNS = [("none", None), ("lb_mv", None), ("lb_ti", None), ("lb_pc", None), ("lb_ad", None),
+        ("tc_dtw", "lb_ti"), ("tc_dtw", "lb_pc")]
+
+
+def _params(P, w, method):
+    return P.SearchParams(window=w, method=P.Method(method))
+
+
+def test_nn_search_small_golden(P):
+    for case in load_cases("search_small"):
+        runs = RUNS if "m1_best_index" in case else [("lb_ti", None)]
+        for k, (method, adv) in enumerate(runs):
+            out = P.nn_search(case["q"], list(case["cands"]), _params(P, case["w"], method),
+                              advanced=None if adv is None else P.Method(adv), dim_range=dr_or_none(case["dr"]))
+            assert out.best_index == case[f"m{k}_best_index"], (method, adv)
+            assert out.best_distance == case[f"m{k}_best_distance"], (method, adv)
+            assert out.dtw_computed + out.dtw_skipped == len(case["cands"])
+
+
+def test_c0_all_methods_golden(P):
+    from paper_2101_07731_b200.datasets import make_workload
+
+    wl = make_workload("C0")
+    cases = [c for c in load_cases("configs") if c["cfg"] == "C0"]
+    index = P.SearchIndex(wl.candidates, dtype="f64")
+    for k, (method, adv) in enumerate(RUNS):
+        res = index.search(wl.queries, _params(P, 12, method), advanced=None if adv is None else P.Method(adv),
+                           dim_range=wl.dim_range)
+        for case in cases:
+            qi = case["qi"]
+            assert res.best_index[qi] == case[f"m{k}_best_index"], (method, adv, qi)
+            assert res.best_distance[qi] == case[f"m{k}_best_distance"], (method, adv, qi)
+        c = res.counters
+        assert np.all(c["dtw_computed"] + c["dtw_skipped"] == len(wl.candidates))
+
+
+def _oracle_check(P, cfg, wi, n_queries, method="lb_mv", advanced=None, dtype=None, rel=0.0):
+    from oracle import oracle as O
+    from paper_2101_07731_b200.datasets import make_workload
+
+    wl = make_workload(cfg)
+    w = wl.spec.windows()[wi]
+    qsel = wl.queries[:n_queries]
+    res = P.SearchIndex(wl.candidates, dtype=dtype or wl.dtype).search(
+        qsel, _params(P, w, method), advanced=None if advanced is None else P.Method(advanced),
+        dim_range=wl.dim_range)
+    outs, _ = O.nn_search_batch(qsel.astype(np.float64), wl.candidates.astype(np.float64),
+                                O.make_params(w, method), advanced, wl.dim_range)
+    for i, o in enumerate(outs):
+        assert res.best_index[i] == o.best_index, (cfg, i)
+        if rel == 0.0:
+            assert res.best_distance[i] == o.best_distance, (cfg, i)
+        else:
+            assert abs(res.best_distance[i] - o.best_distance) <= rel * o.best_distance, (cfg, i)
+    return res
+
+
+def test_c1a_full_parity(P):
+    # all 500 queries, float32 filter + float64 re-score: bit-exact distances
+    _oracle_check(P, "C1", 0, 500, rel=0.0)
+
+
+def test_c1b_parity(P):
+    _oracle_check(P, "C1", 1, 64, rel=0.0)
+
+
+def test_c1_cascades_parity(P):
+    _oracle_check(P, "C1", 0, 32, method="lb_pc", rel=0.0)
+    _oracle_check(P, "C1", 0, 16, method="tc_dtw", advanced="lb_ti", rel=0.0)
+
+
+def test_c2_parity(P):
+    _oracle_check(P, "C2", 0, 16, rel=0.0)
+
+
+def test_c3_parity(P):
+    _oracle_check(P, "C3", 0, 8, rel=0.0)
+
+
+def test_c4_sampled_parity(P):
+    _oracle_check(P, "C4", 0, 4, rel=0.0)
+
+
+# ------------------------------------------------------------- edge cases
+def test_edge_cases(P, rng):
+    from oracle import oracle as O
+
+    def check(q, cands, w, method="lb_mv", dtype="f64"):
+        res = P.SearchIndex(cands, dtype=dtype).search(q[None], _params(P, w, method))
+        outs, _ = O.nn_search_batch(q[None].astype(np.float64), np.asarray(cands, dtype=np.float64),
+                                    O.make_params(w, method), None, None)
+        assert res.best_index[0] == outs[0].best_index
+        assert res.best_distance[0] == outs[0].best_distance
+
+    # n == 1, W >= n, W == 0, d == 1, one candidate, fewer candidates than seeds
+    check(rng.normal(size=(1, 3)), rng.normal(size=(5, 1, 3)), 4)
+    check(rng.normal(size=(12, 1)), rng.normal(size=(7, 12, 1)), 40)
+    check(rng.normal(size=(12, 2)), rng.normal(size=(1, 12, 2)), 0)
+    check(rng.normal(size=(12, 2)), rng.normal(size=(3, 12, 2)), 2)
+    # exact ties: duplicates of the nearest candidate -> lowest index wins
+    base = np.cumsum(rng.normal(size=(40, 20, 3)), axis=1)
+    cands = np.concatenate([base[1:], base[1:], base[1:]])
+    for method in ("none", "lb_mv", "lb_pc", "lb_ti", "lb_ad"):
+        check(base[0], cands, 3, method)
+        check(base[0].astype(np.float32), cands.astype(np.float32), 3, method, dtype="f32")
+    # query identical to a candidate: distance 0
+    check(base[5], base, 3)
+    # constant series everywhere (every distance equal)
+    const = np.ones((64, 16, 2))
+    check(const[0], const, 2)
+    check(const[0].astype(np.float32), const.astype(np.float32), 2, dtype="f32")
+
+
+def test_errors(P, rng):
+    with pytest.raises(P.InvalidInputError):
+        P.nn_search(rng.normal(size=(5, 2)), [], P.SearchParams(window=2))
+    with pytest.raises(P.InvalidInputError):
+        P.nn_search(rng.normal(size=(5, 2)), [rng.normal(size=(5, 2))], P.SearchParams(window=2, method="tc_dtw"))
+    with pytest.raises(P.InvalidInputError):
+        P.dtw_banded(np.zeros((3, 2)), np.zeros((4, 2)), 1)
+    with pytest.raises(P.InvalidInputError):
+        P.SearchIndex(np.zeros((2, 5, 2))).search(np.full((5, 2), np.nan), P.SearchParams(window=1, method="lb_mv"))
+
+
+# ------------------------------------------------------ sharding on 1 GPU
+def test_sharded_combine_equals_single(P):
+    """G logical shards searched separately (global d_best exchanged between
+    the phases, as the NCCL path does) and combined lexicographically equal
+    the single-shard answer."""
+    import torch
+
+    from paper_2101_07731_b200.datasets import make_workload
+    from paper_2101_07731_b200.distributed import shard_bounds
+
+    wl = make_workload("C1", n_candidates=3000, n_queries=64)
+    params = _params(P, 12, "lb_mv")
+    ref = P.SearchIndex(wl.candidates, dtype="f32").search(wl.queries, params)
+    for G in (2, 3, 8):
+        shards = [P.SearchIndex(wl.candidates[a:b], dtype="f32", base=a)
+                  for a, b in (shard_bounds(len(wl.candidates), G, r) for r in range(G))]
+        Q = [s.prepare_queries(wl.queries) for s in shards]
+        states = [s.seed_phase(q, params) for s, q in zip(shards, Q)]
+        dmin = torch.stack([st["dbest"] for st in states]).min(dim=0).values  # the NCCL all-reduce(MIN)
+        for st in states:
+            st["dbest"].copy_(dmin)
+        best = np.full(len(wl.queries), np.inf)
+        idx = np.full(len(wl.queries), -1)
+        for s, st in zip(shards, states):
+            bi, bd, _ = s.finish_phase(st)
+            bi, bd = bi.cpu().numpy(), bd.cpu().numpy()
+            better = (bi >= 0) & ((bd < best) | ((bd == best) & ((idx < 0) | (bi < idx))))
+            best = np.where(better, bd, best)
+            idx = np.where(better, bi, idx)
+        assert np.array_equal(idx, ref.best_index)
+        assert np.array_equal(best, ref.best_distance)
+    del torch
