@@ -26,10 +26,11 @@ namespace tcdtw {
 
 constexpr int kMaxDims = 128;  // numpy's unrecursed pairwise block (PW_BLOCKSIZE)
 
-__device__ __forceinline__ float inf_of(float) { return __int_as_float(0x7f800000); }
-__device__ __forceinline__ double inf_of(double) { return __longlong_as_double(0x7ff0000000000000LL); }
+// +inf, usable from host code (kernel arguments) and device code
+__host__ __device__ __forceinline__ float inf_of(float) { return __builtin_huge_valf(); }
+__host__ __device__ __forceinline__ double inf_of(double) { return __builtin_huge_val(); }
 
-template <typename T> __device__ __forceinline__ T dev_inf() { return inf_of(T(0)); }
+template <typename T> __host__ __device__ __forceinline__ T dev_inf() { return inf_of(T(0)); }
 
 // ---- correctly rounded, never contracted ----------------------------------
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }

@@ -35,6 +35,9 @@
 
 #include <cub/device/device_scan.cuh>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "dispatch.cuh"
 
@@ -1214,6 +1217,15 @@ static int sm_count() {
         if (_s != TCDTW_OK) return _s; \
     } while (0)
 
+// TCDTW_DEBUG=1: synchronise and report after every pipeline stage.
+static void dbg_stage(cudaStream_t st, const char* what) {
+    static const bool on = getenv("TCDTW_DEBUG") != nullptr;
+    if (!on) return;
+    cudaError_t e = cudaStreamSynchronize(st);
+    fprintf(stderr, "[tcdtw] %-24s %s\n", what, cudaGetErrorString(e));
+    fflush(stderr);
+}
+
 template <typename T>
 static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const void* queries, const void* cands,
                           void* ws) {
@@ -1321,10 +1333,12 @@ struct SearchImpl {
                                 at<int32_t>(ws, p.o_bcnt), st));
         if (a.adv == TCDTW_METHOD_LB_TI && p.n > 1)
             TRY(series_steps(dtype, queries, p.Q, p.n, p.d, at<T>(ws, p.o_steps), st));
+        dbg_stage(st, "prep");
         tm.mark(1);
         if (p.has_lb)
             TRY((launch_lbmv_matrix<T, DMAX, EXACT>(at<T>(ws, p.o_upT), at<T>(ws, p.o_loT), at<T>(ws, p.o_candT), p.Q,
                                                     p.N, p.n, p.d, at<T>(ws, p.o_lb), st)));
+        dbg_stage(st, "lb_mv");
         tm.mark(2);
         if (p.S > 0) {
             uint32_t* seeds = at<uint32_t>(ws, p.o_seed);
@@ -1344,11 +1358,13 @@ struct SearchImpl {
             TRY(launch_status());
             fill_kernel<T><<<grid_for(p.Q * p.S, 256), 256, 0, st>>>(at<T>(ws, p.o_seedres), p.Q * p.S, dev_inf<T>());
             TRY(launch_status());
+            dbg_stage(st, "topk+tiles");
             tm.mark(3);
             TRY((launch_dtw<T, DMAX, EXACT>(a, p, stl, p.Q, seeds, at<T>(ws, p.o_seedres), at<int>(ws, p.o_tctr), st)));
         } else {
             tm.mark(3);
         }
+        dbg_stage(st, "seed dtw");
         tm.mark(4);
         if (dbest_out && dbest_out != (void*)a.dbest)
             cudaMemcpyAsync(dbest_out, a.dbest, (size_t)p.Q * sizeof(T), cudaMemcpyDeviceToDevice, st);
@@ -1400,6 +1416,7 @@ struct SearchImpl {
         TRY(launch_status());
         // the number of tiles stays on the device: kernels stop at the first
         // tile past the end (tile_q sentinel), bounded by max_tiles.
+        dbg_stage(st, "compact+tiles");
         int64_t n_tiles = 0;
         cudaMemcpyAsync(&n_tiles, toff + p.Q, 8, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
@@ -1411,8 +1428,10 @@ struct SearchImpl {
                                                                  at<int>(ws, p.o_tctr));
             TRY(launch_status());
         }
+        dbg_stage(st, "advanced");
         tm.mark(6);
         TRY((launch_dtw<T, DMAX, EXACT>(a, p, tl, n_tiles, surv, res, at<int>(ws, p.o_tctr), st)));
+        dbg_stage(st, "dtw");
         tm.mark(7);
         // finalize
         T* minv = at<T>(ws, p.o_minv);
@@ -1452,6 +1471,7 @@ struct SearchImpl {
         fin_output_kernel<T><<<grid_for(p.Q, 256), 256, 0, st>>>(p.Q, p.N, dsc->candidate_base, minv, min64, bidx,
                                                                 a.counters, p.has_lb ? 1 : 0, best_index,
                                                                 best_distance, counters);
+        dbg_stage(st, "finalize");
         tm.mark(8 > TCDTW_PHASES ? TCDTW_PHASES : 8);
         tm.finish();
         return launch_status();
