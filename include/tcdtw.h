@@ -153,7 +153,7 @@ typedef struct tcdtw_search_desc {
 
 #define TCDTW_FLAG_TIMING 1 /* fill desc->phase_ms (synchronises the stream) */
 #define TCDTW_PHASES 8      /* prep, lb_mv, seeds_topk, seeds_dtw, compact, advanced, dtw, finalize */
-#define TCDTW_COUNTERS 8    /* per query: see enum below */
+#define TCDTW_COUNTERS 9    /* per query: see enum below */
 
 enum tcdtw_counter {
     TCDTW_C_DTW_COMPUTED = 0,  /* NnOutcome.dtw_computed (search.py:46-56) */
@@ -163,7 +163,8 @@ enum tcdtw_counter {
     TCDTW_C_ABANDON_COUNT = 4,
     TCDTW_C_DTW_CELLS = 5,     /* DP cells evaluated, as dtw.py:96 counts them */
     TCDTW_C_FINALISTS = 6,     /* candidates re-scored / tie-checked in float64 */
-    TCDTW_C_SURVIVORS = 7      /* entries left after LB_MV */
+    TCDTW_C_SURVIVORS = 7,     /* entries left after LB_MV */
+    TCDTW_C_CELLS_ISSUED = 8   /* DP cells issued by the DTW kernels incl. lockstep waste */
 };
 
 int tcdtw_search_workspace_size(const tcdtw_search_desc *desc, size_t *bytes);

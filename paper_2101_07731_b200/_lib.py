@@ -21,7 +21,7 @@ TCDTW_OK, TCDTW_INVALID_INPUT, TCDTW_CUDA_ERROR, TCDTW_WORKSPACE_TOO_SMALL, TCDT
 F32, F64 = 0, 1
 PHASES = ("prep", "lb_mv", "seeds_topk", "seeds_dtw", "compact", "advanced", "dtw", "finalize")
 COUNTERS = ("dtw_computed", "dtw_skipped", "lb_mv_evals", "advanced_lb_evals", "abandon_count",
-            "dtw_cells", "finalists", "survivors")
+            "dtw_cells", "finalists", "survivors", "cells_issued")
 FLAG_TIMING = 1
 
 _vp = ctypes.c_void_p

@@ -1,0 +1,2120 @@
+#pragma once
+// search_impl.cuh -- the batched 1-NN search (nn_search, search.py:75-180) on B200.
+//
+// Pipeline per call (a batch of Q queries against one shard of N candidates):
+//
+//   prep      query envelopes (lb_mv.py:74-88), planar copies for tiling,
+//             box sets (lb_pc.py:239-261) / query steps (lb_ti.py:51-55)
+//   lb_mv     LB_MV of every (query, candidate) pair: a register-tiled
+//             ALU-bound kernel over planar [t][p][*] operands staged in shared
+//             memory (lb_mv.py:91-107) -> LB matrix (Q, N) in HBM
+//   seeds     per query the S smallest bounds; their exact DTWs seed the
+//             device-resident best-so-far d_best (replaces the reference's
+//             seed from candidate 0, search.py:127-133)
+//   compact   survivors LB <= thr(d_best), written per query in candidate
+//             order (prune rule search.py:144, made order-free, see below)
+//   advanced  LB_PC / LB_TI / LB_AD on survivors in the trigger band
+//             e*d_best < LB_MV (search.py:147-165)
+//   dtw       banded DTW of the survivors with early abandoning against the
+//             live d_best (atomicMin), thread-per-pair (band in registers)
+//             for 2W+1 <= 64, warp-per-pair anti-diagonal wavefront beyond
+//   finalize  lexicographic (distance, index) minimum; in float32 the
+//             finalists are re-scored in EXACT float64.
+//
+// Order-free exactness.  The reference returns the linear-scan argmin with
+// the lowest index winning ties (search.py:144,163,173; dtw.py:97).  Here:
+//   EXACT (float64): every bound and DTW value is bit-identical to the
+//     reference's, so pruning with strict '>' against d_best can never drop
+//     a candidate whose DTW is <= the final best, and the tie rule is applied
+//     by a final lexicographic reduction over completed DTWs.
+//   FAST (float32): every decision carries a margin eps = (2n+d+16)*2^-23
+//     covering float32 rounding of bounds and DTW: prune / abandon iff
+//     value > d_best * (1+3 eps); candidates whose float32 DTW is within
+//     (1+2.5 eps) of the best are re-scored in EXACT float64 on the same
+//     (float32) inputs, and the lexicographic minimum of those is returned.
+//     The answer is therefore the reference's on the float32-rounded data.
+
+#include <cub/device/device_scan.cuh>
+
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+
+#include "common.cuh"
+#include "dispatch.cuh"
+
+namespace tcdtw {
+
+// host wrappers defined in k_pairs.cu
+int series_envelope(int dtype, const void* s, int64_t ns, int n, int d, int w, void* u, void* l,
+                    cudaStream_t st);
+int series_steps(int dtype, const void* s, int64_t ns, int n, int d, void* out, cudaStream_t st);
+int series_box_sets(int dtype, const void* s, int64_t ns, int n, int d, int w, int gw, int levels, int K,
+                    double mcf, const void* dr, void* olo, void* ohi, int32_t* counts, cudaStream_t st);
+
+constexpr int kSeedMax = 32;
+constexpr int kChunk = 2048;  // compaction chunk (candidates per block)
+// Survivor lists are laid out chunk-major: segment (chunk, query) at index
+// chunk * Q + q.  Work tiles are consumed in that order, so the warps of the
+// whole GPU work on one candidate chunk (kChunk series, a few MB) across all
+// queries at a time and read the candidate rows from L2, not HBM.
+constexpr int kTile = 32;     // survivors per work tile (one per lane)
+
+// ----------------------------------------------------------- small helpers
+__host__ __device__ inline int64_t cells_upto(int r, int n, int w) {
+    // sum_{i=0}^{r} (min(n-1, i+w) - max(0, i-w) + 1), dtw.py:96
+    const int64_t R = r;
+    int64_t a = n - 1 - w;  // last i with i + w <= n-1
+    if (a > R) a = R;
+    int64_t s1 = 0;
+    if (a >= 0) s1 = (a + 1) * (int64_t)w + a * (a + 1) / 2;
+    const int64_t s2 = (R - a) * (int64_t)(n - 1);
+    int64_t s3 = 0;
+    if (R >= w) s3 = (R - w) * (R - w + 1) / 2;
+    return (R + 1) + s1 + s2 - s3;
+}
+
+struct Margins {
+    float prune;  // d_best multiplier for prune / abandon thresholds
+    float fin;    // best multiplier for finalists
+};
+
+template <typename T>
+__device__ __forceinline__ T scale_up(T v, float m);
+template <>
+__device__ __forceinline__ float scale_up<float>(float v, float m) {
+    return __fmul_ru(v, m);
+}
+template <>
+__device__ __forceinline__ double scale_up<double>(double v, float) {
+    return v;  // EXACT: no margin
+}
+
+// ------------------------------------------------------- planar transpose
+// [s][t][p] -> [t*d+p][s]: operands of the tiled LB_MV kernel.
+template <typename T>
+__global__ void planar_kernel(const T* __restrict__ in, int64_t S, int rows, T* __restrict__ out) {
+    __shared__ T tile[32][33];
+    const int64_t s0 = (int64_t)blockIdx.x * 32;
+    const int r0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t s = s0 + k;
+        const int r = r0 + tx;
+        tile[k][tx] = (s < S && r < rows) ? in[s * rows + r] : T(0);
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        const int r = r0 + k;
+        const int64_t s = s0 + tx;
+        if (r < rows && s < S) out[(int64_t)r * S + s] = tile[tx][k];
+    }
+}
+
+template <typename T>
+int planarize(const T* in, int64_t S, int rows, T* out, cudaStream_t st) {
+    dim3 grid((unsigned)((S + 31) / 32), (unsigned)((rows + 31) / 32));
+    if (grid.y > 65535) return TCDTW_NOT_SUPPORTED;
+    planar_kernel<T><<<grid, 256, 0, st>>>(in, S, rows, out);
+    return launch_status();
+}
+
+// ------------------------------------------------------------ LB_MV matrix
+// Block = 16 x 16 threads, tile QT = 16*M queries x CT = 16*M candidates,
+// TC time steps staged per round.  Each thread accumulates M x M pairs,
+// strictly sequentially over t (the reference's cumsum order, which keeps
+// LB <= DTW exact in float64).
+//
+// With UB, the same pass also accumulates the diagonal-path cost
+// sum_t ||q_t - c_t||: the cost of one admissible warping path, hence an
+// UPPER bound of the banded DTW (exactly so in float64, where it is the
+// DP's own sum along that path).  Its per-query minimum seeds d_best and its
+// smallest entries pick the seed candidates.
+template <typename T, int DMAX, bool EXACT>
+struct MvTile {
+    static constexpr int M = EXACT ? (DMAX <= 8 ? 2 : 1) : 4;
+    static constexpr int QT = 16 * M;
+    static constexpr int CT = 16 * M;
+};
+
+template <typename T, int DMAX, bool EXACT, bool UB>
+__global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ UT, const T* __restrict__ LT,
+                                                          const T* __restrict__ QTP, const T* __restrict__ CT_,
+                                                          int64_t Q, int64_t N, int n, int d, int TC,
+                                                          T* __restrict__ out, T* __restrict__ ub_out) {
+    using Tile = MvTile<T, DMAX, EXACT>;
+    constexpr int M = Tile::M, QT = Tile::QT, CTL = Tile::CT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* us = reinterpret_cast<T*>(smem_raw);
+    T* ls = us + (size_t)TC * d * QT;
+    T* cs = ls + (size_t)TC * d * QT;
+    T* qs = cs + (size_t)TC * d * CTL;  // UB only
+    const int tid = threadIdx.x;
+    const int tq = tid & 15, tc = tid >> 4;
+    // query tiles vary fastest: concurrently resident blocks share one
+    // candidate tile, so each candidate byte leaves HBM once per batch and the
+    // (small) envelope tiles are re-read from L2.
+    const int64_t nqt = (Q + QT - 1) / QT;
+    const int64_t q0 = ((int64_t)blockIdx.x % nqt) * QT;
+    const int64_t c0 = ((int64_t)blockIdx.x / nqt) * CTL;
+    T total[M][M], ubt[M][M];
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int j = 0; j < M; ++j) total[i][j] = ubt[i][j] = T(0);
+
+    for (int t0 = 0; t0 < n; t0 += TC) {
+        const int tcn = (n - t0) < TC ? (n - t0) : TC;
+        const int rows = tcn * d;
+        const int64_t rbase = (int64_t)t0 * d;
+        for (int e = tid; e < rows * QT; e += 256) {
+            const int r = e / QT, qq = e - (e / QT) * QT;
+            const int64_t q = q0 + qq;
+            const bool ok = q < Q;
+            us[e] = ok ? UT[(rbase + r) * Q + q] : T(0);
+            ls[e] = ok ? LT[(rbase + r) * Q + q] : T(0);
+            if constexpr (UB) qs[e] = ok ? QTP[(rbase + r) * Q + q] : T(0);
+        }
+        for (int e = tid; e < rows * CTL; e += 256) {
+            const int r = e / CTL, cc = e - (e / CTL) * CTL;
+            const int64_t c = c0 + cc;
+            cs[e] = c < N ? CT_[(rbase + r) * N + c] : T(0);
+        }
+        __syncthreads();
+        for (int tt = 0; tt < tcn; ++tt) {
+            if constexpr (EXACT) {
+                T sq[M][M][DMAX], sd[M][M][DMAX];
+#pragma unroll
+                for (int p = 0; p < DMAX; ++p) {
+                    if (p < d) {
+                        const int r = tt * d + p;
+                        T u[M], l[M], c[M], qv[M];
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            u[i] = us[r * QT + tq * M + i];
+                            l[i] = ls[r * QT + tq * M + i];
+                            c[i] = cs[r * CTL + tc * M + i];
+                            if constexpr (UB) qv[i] = qs[r * QT + tq * M + i];
+                        }
+#pragma unroll
+                        for (int i = 0; i < M; ++i)
+#pragma unroll
+                            for (int j = 0; j < M; ++j) {
+                                const T hi = tmax(sub_rn(c[j], u[i]), T(0));
+                                const T lo = tmax(sub_rn(l[i], c[j]), T(0));
+                                sq[i][j][p] = add_rn(mul_rn(hi, hi), mul_rn(lo, lo));
+                                if constexpr (UB) {
+                                    const T df = sub_rn(qv[i], c[j]);  // cost_band order: q - c
+                                    sd[i][j][p] = mul_rn(df, df);
+                                }
+                            }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < M; ++i)
+#pragma unroll
+                            for (int j = 0; j < M; ++j) sq[i][j][p] = sd[i][j][p] = T(0);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < M; ++i)
+#pragma unroll
+                    for (int j = 0; j < M; ++j) {
+                        total[i][j] = add_rn(total[i][j], sqrt_rn(np_sum<T, DMAX>(sq[i][j], d)));
+                        if constexpr (UB) ubt[i][j] = add_rn(ubt[i][j], sqrt_rn(np_sum<T, DMAX>(sd[i][j], d)));
+                    }
+            } else {
+                T s[M][M], sd[M][M];
+#pragma unroll
+                for (int i = 0; i < M; ++i)
+#pragma unroll
+                    for (int j = 0; j < M; ++j) s[i][j] = sd[i][j] = T(0);
+                for (int p = 0; p < d; ++p) {
+                    const int r = tt * d + p;
+                    T u[M], l[M], c[M], qv[M];
+                    if constexpr (M == 4 && sizeof(T) == 4) {
+                        const float4 u4 = *reinterpret_cast<const float4*>(us + r * QT + tq * 4);
+                        const float4 l4 = *reinterpret_cast<const float4*>(ls + r * QT + tq * 4);
+                        const float4 c4 = *reinterpret_cast<const float4*>(cs + r * CTL + tc * 4);
+                        u[0] = u4.x; u[1] = u4.y; u[2] = u4.z; u[3] = u4.w;
+                        l[0] = l4.x; l[1] = l4.y; l[2] = l4.z; l[3] = l4.w;
+                        c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+                        if constexpr (UB) {
+                            const float4 q4 = *reinterpret_cast<const float4*>(qs + r * QT + tq * 4);
+                            qv[0] = q4.x; qv[1] = q4.y; qv[2] = q4.z; qv[3] = q4.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            u[i] = us[r * QT + tq * M + i];
+                            l[i] = ls[r * QT + tq * M + i];
+                            c[i] = cs[r * CTL + tc * M + i];
+                            if constexpr (UB) qv[i] = qs[r * QT + tq * M + i];
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < M; ++i)
+#pragma unroll
+                        for (int j = 0; j < M; ++j) {
+                            // u >= l, so at most one of (c-u, l-c) is positive
+                            const T dev = tmax(tmax(c[j] - u[i], l[i] - c[j]), T(0));
+                            s[i][j] = fma(dev, dev, s[i][j]);
+                            if constexpr (UB) {
+                                const T df = qv[i] - c[j];
+                                sd[i][j] = fma(df, df, sd[i][j]);
+                            }
+                        }
+                }
+#pragma unroll
+                for (int i = 0; i < M; ++i)
+#pragma unroll
+                    for (int j = 0; j < M; ++j) {
+                        total[i][j] += fast_sqrt(s[i][j]);
+                        if constexpr (UB) ubt[i][j] += fast_sqrt(sd[i][j]);
+                    }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const int64_t q = q0 + tq * M + i;
+        if (q >= Q) continue;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            const int64_t c = c0 + tc * M + j;
+            if (c < N) {
+                out[q * N + c] = total[i][j];
+                if constexpr (UB) ub_out[q * N + c] = ubt[i][j];
+            }
+        }
+    }
+}
+
+template <typename T, int DMAX, bool EXACT>
+int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int64_t Q, int64_t N, int n, int d,
+                       T* out, T* ub_out, cudaStream_t st) {
+    using Tile = MvTile<T, DMAX, EXACT>;
+    const bool ub = ub_out != nullptr;
+    const size_t per_t = (size_t)d * ((ub ? 3 : 2) * Tile::QT + Tile::CT) * sizeof(T);
+    int TC = (int)((48 * 1024) / per_t);
+    TC = TC < 1 ? 1 : (TC > 16 ? 16 : TC);
+    TC = TC > n ? n : TC;
+    const size_t smem = per_t * TC;
+    auto kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true> : lbmv_matrix_kernel<T, DMAX, EXACT, false>;
+    if (smem > 48 * 1024) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return TCDTW_CUDA_ERROR;
+    }
+    const int64_t nqt = (Q + Tile::QT - 1) / Tile::QT;
+    const int64_t nct = (N + Tile::CT - 1) / Tile::CT;
+    if (nqt * nct > 2147483647LL) return TCDTW_NOT_SUPPORTED;
+    const unsigned grid = (unsigned)(nqt * nct);
+    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out);
+    return launch_status();
+}
+
+// ------------------------------------------------------------ seeds (top-S)
+template <typename T, int S>
+__global__ void __launch_bounds__(256) topk_kernel(const T* __restrict__ lb, int64_t N, int s_eff, T* __restrict__ dbest,
+                                                   uint32_t* __restrict__ seeds, int32_t* __restrict__ seed_cnt) {
+    const int64_t q = blockIdx.x;
+    const T* row = lb + q * N;
+    T bv[S];
+    uint32_t bi[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+        bv[k] = dev_inf<T>();
+        bi[k] = 0xffffffffu;
+    }
+    for (int64_t c = threadIdx.x; c < N; c += blockDim.x) {
+        const T v = row[c];
+        if (v < bv[S - 1]) {
+            bv[S - 1] = v;
+            bi[S - 1] = (uint32_t)c;
+#pragma unroll
+            for (int k = S - 1; k > 0; --k) {
+                if (bv[k] < bv[k - 1]) {
+                    T tv = bv[k]; bv[k] = bv[k - 1]; bv[k - 1] = tv;
+                    uint32_t ti = bi[k]; bi[k] = bi[k - 1]; bi[k - 1] = ti;
+                }
+            }
+        }
+    }
+    __shared__ T sv[8];
+    __shared__ uint32_t si[8];
+    __shared__ T win_v;
+    __shared__ uint32_t win_i;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int r = 0; r < s_eff; ++r) {
+        T v = bv[0];
+        uint32_t i = bi[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const T ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const uint32_t oi = __shfl_xor_sync(0xffffffffu, i, o);
+            if (ov < v || (ov == v && oi < i)) { v = ov; i = oi; }
+        }
+        if (lane == 0) { sv[wid] = v; si[wid] = i; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            T bvv = sv[0];
+            uint32_t bii = si[0];
+            for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+                if (sv[k] < bvv || (sv[k] == bvv && si[k] < bii)) { bvv = sv[k]; bii = si[k]; }
+            win_v = bvv;
+            win_i = bii;
+            seeds[q * S + r] = bii;
+            // keys are diagonal-path upper bounds: the smallest one bounds the
+            // final nearest-neighbour distance from above
+            if (r == 0 && dbest && bvv < dbest[q]) dbest[q] = bvv;
+        }
+        __syncthreads();
+        if (bi[0] == win_i && win_i != 0xffffffffu) {
+#pragma unroll
+            for (int k = 0; k < S - 1; ++k) { bv[k] = bv[k + 1]; bi[k] = bi[k + 1]; }
+            bv[S - 1] = dev_inf<T>();
+            bi[S - 1] = 0xffffffffu;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) seed_cnt[q] = s_eff;
+}
+
+// --------------------------------------------------------------- work tiles
+struct Tiles {
+    uint32_t* q;      // query of the tile
+    int64_t* begin;   // first entry
+    int32_t* len;     // entries (<= 32)
+};
+
+// seed list: one tile per query (S <= 32 entries at q*S)
+static __global__ void seed_tiles_kernel(int64_t Q, int S, const int32_t* __restrict__ seed_cnt, Tiles t) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < Q; q += (int64_t)gridDim.x * blockDim.x) {
+        t.q[q] = (uint32_t)q;
+        t.begin[q] = q * S;
+        t.len[q] = seed_cnt[q];
+    }
+}
+
+// ------------------------------------------------------------- compaction
+template <typename T>
+__device__ __forceinline__ bool keep_pred(const T* __restrict__ lbrow, int64_t c, T thr, bool all,
+                                          const uint32_t* seeds_s, int ns) {
+    if (!all) {
+        if (!(lbrow[c] <= thr)) return false;
+    }
+    for (int k = 0; k < ns; ++k)
+        if (seeds_s[k] == (uint32_t)c) return false;
+    return true;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) compact_count_kernel(const T* __restrict__ lb, int64_t N, int n_chunks,
+                                                            const T* __restrict__ dbest, Margins mg, bool all,
+                                                            const uint32_t* __restrict__ seeds, const int32_t* __restrict__ seed_cnt,
+                                                            int S, int64_t* __restrict__ chunk_cnt) {
+    const int64_t q = blockIdx.y;
+    const int chunk = blockIdx.x;
+    __shared__ uint32_t sd[kSeedMax];
+    __shared__ int wsum[8];
+    const int ns = S > 0 ? seed_cnt[q] : 0;
+    if (threadIdx.x < ns) sd[threadIdx.x] = seeds[q * S + threadIdx.x];
+    __syncthreads();
+    const T thr = all ? T(0) : scale_up<T>(dbest[q], mg.prune);
+    const T* row = lb ? lb + q * N : nullptr;
+    const int64_t c0 = (int64_t)chunk * kChunk;
+    const int64_t c1 = c0 + kChunk < N ? c0 + kChunk : N;
+    int cnt = 0;
+    for (int64_t c = c0 + threadIdx.x; c < c1; c += 256) cnt += keep_pred<T>(row, c, thr, all, sd, ns) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int k = 0; k < 8; ++k) s += wsum[k];
+        chunk_cnt[(int64_t)chunk * gridDim.y + q] = s;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) compact_write_kernel(const T* __restrict__ lb, int64_t N, int n_chunks,
+                                                            const T* __restrict__ dbest, Margins mg, bool all,
+                                                            const uint32_t* __restrict__ seeds, const int32_t* __restrict__ seed_cnt,
+                                                            int S, const int64_t* __restrict__ chunk_off,
+                                                            uint32_t* __restrict__ surv, T* __restrict__ res) {
+    const int64_t q = blockIdx.y;
+    const int chunk = blockIdx.x;
+    __shared__ uint32_t sd[kSeedMax];
+    __shared__ int wsum[8];
+    __shared__ int64_t base_s;
+    const int ns = S > 0 ? seed_cnt[q] : 0;
+    if (threadIdx.x < ns) sd[threadIdx.x] = seeds[q * S + threadIdx.x];
+    if (threadIdx.x == 0) base_s = chunk_off[(int64_t)chunk * gridDim.y + q];
+    __syncthreads();
+    const T thr = all ? T(0) : scale_up<T>(dbest[q], mg.prune);
+    const T* row = lb ? lb + q * N : nullptr;
+    const int64_t c0 = (int64_t)chunk * kChunk;
+    const int64_t c1 = c0 + kChunk < N ? c0 + kChunk : N;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t base = base_s;
+    for (int64_t cb = c0; cb < c1; cb += 256) {
+        const int64_t c = cb + threadIdx.x;
+        const bool k = c < c1 && keep_pred<T>(row, c, thr, all, sd, ns);
+        const unsigned bal = __ballot_sync(0xffffffffu, k);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        int before = 0, tot = 0;
+        for (int w2 = 0; w2 < 8; ++w2) {
+            before += (w2 < wid) ? wsum[w2] : 0;
+            tot += wsum[w2];
+        }
+        if (k) {
+            const int64_t pos = base + before + __popc(bal & ((1u << lane) - 1u));
+            surv[pos] = (uint32_t)c;
+            res[pos] = dev_inf<T>();
+        }
+        base += tot;
+        __syncthreads();
+    }
+}
+
+// per-(chunk, query) survivor segments -> tile counts; then fill
+static __global__ void seg_tiles_count_kernel(int64_t Q, int n_chunks, const int64_t* __restrict__ chunk_off,
+                                       int64_t* __restrict__ tile_cnt, int64_t* __restrict__ counters) {
+    const int64_t n_seg = Q * n_chunks;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_seg; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cnt = chunk_off[g + 1] - chunk_off[g];
+        tile_cnt[g] = (cnt + kTile - 1) / kTile;
+        if (cnt) atomicAdd(reinterpret_cast<unsigned long long*>(counters + (g % Q) * TCDTW_COUNTERS + TCDTW_C_SURVIVORS),
+                           (unsigned long long)cnt);
+    }
+}
+
+static __global__ void seg_tiles_fill_kernel(int64_t Q, int n_chunks, const int64_t* __restrict__ chunk_off,
+                                      const int64_t* __restrict__ tile_off, Tiles t) {
+    const int64_t n_seg = Q * n_chunks;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_seg; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = chunk_off[g], e = chunk_off[g + 1];
+        const int64_t t0 = tile_off[g];
+        const int64_t nt = (e - b + kTile - 1) / kTile;
+        for (int64_t k = 0; k < nt; ++k) {
+            const int64_t bb = b + k * kTile;
+            t.q[t0 + k] = (uint32_t)(g % Q);
+            t.begin[t0 + k] = bb;
+            t.len[t0 + k] = (int32_t)((e - bb) < kTile ? (e - bb) : kTile);
+        }
+    }
+}
+
+// ------------------------------------------------- search-wide arguments
+template <typename T>
+struct SArgs {
+    const T* queries;     // (Q, n, d)
+    const T* cands;       // (N, n, d)
+    const T* lb;          // (Q, N) LB_MV or nullptr
+    const T* env_up;      // (Q, n, d) query envelopes (nullptr without LB_MV)
+    const T* env_lo;
+    T* dbest;             // (Q,)
+    const T* box_lo;      // (Q, G, K, d)
+    const T* box_hi;
+    const T* qsteps;      // (Q, n-1)
+    int64_t* counters;    // (Q, TCDTW_COUNTERS)
+    int64_t N;
+    int n, d, w, G, K, gw, period;
+    int method, adv;
+    float trigger;
+    Margins mg;
+    bool abandon;         // false for Method.NONE (search.py:135)
+    T casc_lo, casc_hi, casc_thr;  // cascaded-abandon slack (see dtw_tpp_kernel)
+};
+
+__device__ __forceinline__ void warp_add_counter(int64_t* ctr, int64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v != 0) atomicAdd(reinterpret_cast<unsigned long long*>(ctr), (unsigned long long)v);
+}
+
+// ----------------------------------------- DTW, thread per pair (2W+1 <= BMAX)
+// Rows = candidate points (one per lane, streamed from HBM), columns = the
+// tile's query, staged once per warp in shared memory with W points of +inf
+// padding on both sides, so every lane reads the same address (broadcast).
+// The row's band lives in registers; DTW is symmetric (test_dtw.py:196-207),
+// and abandoning on candidate rows is as sound as on query rows (every
+// warping path crosses every row).
+template <typename T, int DMAX, int BMAX, bool EXACT>
+__global__ void __launch_bounds__(256) dtw_tpp_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
+                                                      const uint32_t* __restrict__ cand_of, T* __restrict__ res,
+                                                      int* __restrict__ tile_ctr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int VEC = 16 / sizeof(T);
+    const int n = a.n, d = a.d, w = a.w, B = 2 * w + 1;
+    const int DP = (d + VEC - 1) / VEC * VEC;
+    const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* qs = reinterpret_cast<T*>(smem_raw) + (size_t)wib * (n + 2 * w) * DP;
+    const T INF = dev_inf<T>();
+    int64_t cached_q = -1;
+    while (true) {
+        int64_t tile = 0;
+        if (lane == 0) tile = atomicAdd(tile_ctr, 1);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile >= n_tiles) break;
+        const int64_t q = tl.q[tile];
+        const int64_t e0 = tl.begin[tile];
+        const int len = tl.len[tile];
+        if (q != cached_q) {
+            __syncwarp();
+            const T* qsrc = a.queries + q * (int64_t)n * d;
+            for (int e = lane; e < (n + 2 * w) * DP; e += 32) {
+                const int r = e / DP, p = e - (e / DP) * DP;
+                const int j = r - w;
+                T v = T(0);
+                if (p < d) v = (j >= 0 && j < n) ? qsrc[(int64_t)j * d + p] : INF;
+                qs[e] = v;
+            }
+            cached_q = q;
+            __syncwarp();
+        }
+        const bool has = lane < len;
+        const int64_t ent = e0 + lane;
+        const int64_t c = has ? (int64_t)cand_of[ent] : 0;
+        bool active = has;
+        if (has && res[ent] < T(0)) active = false;  // pruned by the advanced bound
+        const T* crow = a.cands + c * (int64_t)n * d;
+        T band[BMAX];
+#pragma unroll
+        for (int k = 0; k < BMAX; ++k) band[k] = (k == w) ? T(0) : INF;
+        T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg.prune) : INF;
+        bool done = !active;
+        int stop_row = n - 1;
+        bool abandoned = false;
+        T cpt[DMAX], cnext[DMAX];
+        load_point<T, DMAX>(cpt, crow, d);
+        // Cascaded abandoning: every warping path visits every later row at a
+        // cost >= that row's LB_MV term, so DTW >= rowmin_i + sum_{r>i} term_r
+        // (the LB_MV row sum is LB[q][c]).  The suffix is estimated from below
+        // with the relative slack a.casc (rounding of both sums).
+        const bool casc = a.lb != nullptr && a.abandon;
+        const T lbtot = (casc && active) ? a.lb[q * a.N + c] : T(0);
+        const T* eu = casc ? a.env_up + q * (int64_t)n * d : nullptr;
+        const T* el = casc ? a.env_lo + q * (int64_t)n * d : nullptr;
+        T prefix = T(0);
+        int iters = 0;
+        for (int i = 0; i < n; ++i) {
+            ++iters;
+            if (i + 1 < n) load_point<T, DMAX>(cnext, crow + (int64_t)(i + 1) * d, d);
+            const T* qrow = qs + (size_t)i * DP;
+            T left = INF, rmin = INF;
+#pragma unroll
+            for (int k = 0; k < BMAX; ++k) {
+                if (k < B) {
+                    const T* qp = qrow + (size_t)k * DP;
+                    T cost;
+                    if constexpr (EXACT) {
+                        cost = dist_exact<T, DMAX>(cpt, qp, d);
+                    } else {
+                        T s = T(0);
+#pragma unroll
+                        for (int v = 0; v < DMAX / VEC; ++v) {
+                            if (v * VEC < d) {
+                                const float4 q4 = *reinterpret_cast<const float4*>(qp + v * VEC);
+                                const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                                for (int u = 0; u < VEC; ++u) {
+                                    if (v * VEC + u < d) {
+                                        const T df = cpt[v * VEC + u] - qv[u];
+                                        s = fma(df, df, s);
+                                    }
+                                }
+                            }
+                        }
+                        cost = fast_sqrt(s);
+                    }
+                    const T up = (k + 1 < BMAX) ? band[k + 1 < BMAX ? k + 1 : 0] : INF;
+                    const T best = tmin(tmin(up, band[k]), left);
+                    const T v = EXACT ? add_rn(cost, best) : cost + best;
+                    band[k] = v;
+                    left = v;
+                    rmin = tmin(rmin, v);
+                }
+            }
+            T bound = rmin;
+            if (casc) {
+                T t2 = T(0);
+#pragma unroll
+                for (int p = 0; p < DMAX; ++p) {
+                    if (p < d) {
+                        const T dv = tmax(tmax(cpt[p] - __ldg(eu + (int64_t)i * d + p),
+                                               __ldg(el + (int64_t)i * d + p) - cpt[p]), T(0));
+                        t2 = fma(dv, dv, t2);
+                    }
+                }
+                prefix += fast_sqrt(t2);
+                const T suf = tmax(lbtot * a.casc_lo - prefix * a.casc_hi, T(0));
+                bound = rmin + suf;
+            }
+            if (!done && (rmin > thr || bound > thr * a.casc_thr)) {
+                done = true;
+                abandoned = true;
+                stop_row = i;
+            }
+            if (__all_sync(0xffffffffu, done)) break;
+            if ((i & 7) == 7 && a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg.prune);
+#pragma unroll
+            for (int p = 0; p < DMAX; ++p) cpt[p] = cnext[p];
+        }
+        T fin = INF;
+#pragma unroll
+        for (int k = 0; k < BMAX; ++k)
+            if (k == w) fin = band[k];
+        if (active && !abandoned && fin > thr) {  // dtw.py:101-102
+            abandoned = true;
+            stop_row = n - 1;
+        }
+        if (active) res[ent] = abandoned ? INF : fin;
+        // best-so-far update and counters (warp-aggregated; one query per tile)
+        T m = (active && !abandoned) ? fin : INF;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = tmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0 && m < INF) atomic_min_nonneg<T>(a.dbest + q, m);
+        int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
+        warp_add_counter(ctr + TCDTW_C_DTW_COMPUTED, active ? 1 : 0);
+        warp_add_counter(ctr + TCDTW_C_ABANDON_COUNT, (active && abandoned) ? 1 : 0);
+        warp_add_counter(ctr + TCDTW_C_DTW_CELLS, active ? cells_upto(stop_row, n, w) : 0);
+        if (lane == 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_CELLS_ISSUED),
+                      (unsigned long long)iters * B * 32);
+    }
+}
+
+// ------------------------------------ DTW, lane per pair, no lockstep
+// Specialised for small (d, 2W+1): each lane keeps its own pair's band AND
+// the query window (2W+1 points) in registers and advances its own row, so
+// a lane whose DTW is abandoned refills at once from the warp's reservoir of
+// work tiles instead of idling until the slowest lane of the warp finishes.
+// Rows = candidate points; the window slides one query point per row.
+template <typename T, int D>
+__device__ __forceinline__ T dist_reg(const T (&a)[D], const T (&b)[D]) {
+    if constexpr (sizeof(T) == 8) {
+        T sq[D];
+#pragma unroll
+        for (int p = 0; p < D; ++p) {
+            const T df = sub_rn(a[p], b[p]);
+            sq[p] = mul_rn(df, df);
+        }
+        return sqrt_rn(np_sum<T, D>(sq, D));
+    } else {
+        T s = T(0);
+#pragma unroll
+        for (int p = 0; p < D; ++p) {
+            const T df = a[p] - b[p];
+            s = fma(df, df, s);
+        }
+        return fast_sqrt(s);
+    }
+}
+
+template <typename T, int D>
+__device__ __forceinline__ void load_pt(T (&a)[D], const T* __restrict__ src) {
+#pragma unroll
+    for (int p = 0; p < D; ++p) a[p] = __ldg(src + p);
+}
+
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
+template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
+
+// rows of a (n, D) series per 16-byte-aligned block: 16 / gcd(16, D*sizeof(T))
+template <typename T, int D>
+constexpr int rows_per_block() {
+    constexpr int b = D * (int)sizeof(T);
+    constexpr int g = (b % 16 == 0) ? 16 : ((b % 8 == 0) ? 8 : 4);
+    return 16 / g;
+}
+
+template <typename T> struct Vec8;
+template <> struct Vec8<float> { using type = float2; };
+template <> struct Vec8<double> { using type = double2; };
+
+// Loads of two consecutive candidate rows (2D values) starting at an even row:
+// 16-byte vectors when 2D*sizeof(T) is a multiple of 16, else 8-byte ones.
+template <typename T, int D>
+struct PairLoad {
+    static constexpr bool v16 = ((2 * D * (int)sizeof(T)) % 16) == 0;
+    using V = typename std::conditional<v16, typename Vec16<T>::type, typename Vec8<T>::type>::type;
+    static constexpr int per = (int)(sizeof(V) / sizeof(T));
+    static constexpr int nv = 2 * D / per;
+};
+
+// One DTW step over two consecutive rows (i, i+1) of one lane's pair.  The
+// cells (i, j) and (i+1, j) share query column j, so every window point read
+// from the ring serves two cells, and the two rows' min chains interleave
+// (skewed by one column): half the shared-memory traffic, twice the ILP of a
+// row-at-a-time sweep.  P holds row i-1 on entry and row i on exit; N
+// receives row i+1.
+template <typename T, int D, int B, bool EXACT>
+__device__ __forceinline__ void dtw_step2(T (&P)[B], T (&N)[B], const T (&c0)[D], const T (&c1)[D],
+                                          const typename Vec8<T>::type* __restrict__ ring, int h,
+                                          const T (&x1)[D], T& rmin0, T& rmin1) {
+    using T2 = typename Vec8<T>::type;
+    constexpr int DP = (D + 1) / 2;
+    const T INF = dev_inf<T>();
+    const T2* base0 = ring + h * DP * 32;
+    const T2* base1 = base0 - B * DP * 32;
+    const int lim = B - h;
+    T left0 = INF, left1 = INF;
+    rmin0 = INF;
+    rmin1 = INF;
+#pragma unroll
+    for (int s = 0; s <= B; ++s) {
+        T x[D];
+        if (s < B) {
+            const T2* qp = (s < lim ? base0 : base1) + s * DP * 32;
+#pragma unroll
+            for (int pp = 0; pp < DP; ++pp) {
+                const T2 v = qp[pp * 32];
+                x[2 * pp] = v.x;
+                if (2 * pp + 1 < D) x[2 * pp + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int p = 0; p < D; ++p) x[p] = x1[p];
+        }
+        if (s < B) {  // row i, slot s
+            T cost;
+            if constexpr (EXACT) {
+                T sq[D];
+#pragma unroll
+                for (int p = 0; p < D; ++p) {
+                    const T df = sub_rn(c0[p], x[p]);
+                    sq[p] = mul_rn(df, df);
+                }
+                cost = sqrt_rn(np_sum<T, D>(sq, D));
+            } else {
+                T acc = T(0);
+#pragma unroll
+                for (int p = 0; p < D; ++p) {
+                    const T df = c0[p] - x[p];
+                    acc = fma(df, df, acc);
+                }
+                cost = fast_sqrt(acc);
+            }
+            const T up = (s + 1 < B) ? P[s + 1 < B ? s + 1 : 0] : INF;
+            const T best = tmin(tmin(up, P[s]), left0);
+            const T v = EXACT ? add_rn(cost, best) : cost + best;
+            P[s] = v;
+            left0 = v;
+            rmin0 = tmin(rmin0, v);
+        }
+        if (s >= 1) {  // row i+1, slot s-1: up = (i, j) just computed, diag = (i, j-1)
+            T cost;
+            if constexpr (EXACT) {
+                T sq[D];
+#pragma unroll
+                for (int p = 0; p < D; ++p) {
+                    const T df = sub_rn(c1[p], x[p]);
+                    sq[p] = mul_rn(df, df);
+                }
+                cost = sqrt_rn(np_sum<T, D>(sq, D));
+            } else {
+                T acc = T(0);
+#pragma unroll
+                for (int p = 0; p < D; ++p) {
+                    const T df = c1[p] - x[p];
+                    acc = fma(df, df, acc);
+                }
+                cost = fast_sqrt(acc);
+            }
+            const T up = (s < B) ? P[s < B ? s : 0] : INF;
+            const T best = tmin(tmin(up, P[s - 1 >= 0 ? s - 1 : 0]), left1);
+            const T v = EXACT ? add_rn(cost, best) : cost + best;
+            N[s - 1 >= 0 ? s - 1 : 0] = v;
+            left1 = v;
+            rmin1 = tmin(rmin1, v);
+        }
+    }
+}
+
+template <typename T, int D, int B, bool EXACT, bool VEC>
+__global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
+                                                      const uint32_t* __restrict__ cand_of, T* __restrict__ res,
+                                                      int* __restrict__ tile_ctr) {
+    constexpr int W = (B - 1) / 2;
+    constexpr int DP = (D + 1) / 2;     // coordinate pairs per point
+    constexpr bool QV = (D % 2 == 0);   // query/envelope rows as pairs
+    using T2 = typename Vec8<T>::type;
+    using PL = PairLoad<T, D>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int n = a.n;
+    const int lane = threadIdx.x & 31;
+    // per-lane query window ring, lane-minor pairs: slot s, pair pp of this
+    // lane at ring[(s*DP + pp)*32] -> conflict-free 64/128-bit accesses.
+    // Column c lives in slot (c + W) mod B.
+    T2* ring = reinterpret_cast<T2*>(smem_raw) + (size_t)(threadIdx.x >> 5) * B * DP * 32 + lane;
+    // per-warp copy of the current tile query's columns 0..W (the window of
+    // row 0), staged once per tile so new pairs fill their ring from smem
+    T2* qstage = reinterpret_cast<T2*>(smem_raw) + (size_t)(blockDim.x >> 5) * B * DP * 32 +
+                 (size_t)(threadIdx.x >> 5) * (W + 1) * DP;
+    int staged_q = -1;
+    const unsigned FULL = 0xffffffffu;
+    const T INF = dev_inf<T>();
+    const bool casc = a.lb != nullptr && a.abandon;
+    // warp reservoir (uniform) with per-tile prefetch held one entry per lane
+    int64_t t_begin = 0;
+    int t_q = -1, t_len = 0, t_next = 0;
+    bool exhausted = false;
+    T t_thr_raw = INF;  // best-so-far as loaded; the margin is applied at use
+    uint32_t pf_c = 0;
+    T pf_lb = T(0), pf_res = T(0);
+    T pf_pair[2 * D];
+    // lane state
+    bool busy = false;
+    int64_t ent = 0;
+    int q = -1, i = 0, since = 0, h = 0;
+    const T* crow = nullptr;
+    const T* qser = nullptr;
+    T bandA[B], bandB[B];
+    T c0[D], c1[D], n0[D], n1[D];
+    T thr = INF, thr_pend_raw = INF, lbtot = T(0), prefix = T(0);
+    T x1[D], x2[D];             // query columns i+W+1, i+W+2 (loaded one step ahead)
+    T eu0[D], el0[D], eu1[D], el1[D];  // envelope rows i, i+1 (loaded one step ahead)
+    int cq = -1;
+    long long c_comp = 0, c_ab = 0, c_cells = 0, c_issued = 0;
+    auto flush = [&]() {
+        if (cq >= 0) {
+            unsigned long long* ctr = reinterpret_cast<unsigned long long*>(a.counters + (int64_t)cq * TCDTW_COUNTERS);
+            if (c_comp) atomicAdd(ctr + TCDTW_C_DTW_COMPUTED, (unsigned long long)c_comp);
+            if (c_ab) atomicAdd(ctr + TCDTW_C_ABANDON_COUNT, (unsigned long long)c_ab);
+            if (c_cells) atomicAdd(ctr + TCDTW_C_DTW_CELLS, (unsigned long long)c_cells);
+            if (c_issued) atomicAdd(ctr + TCDTW_C_CELLS_ISSUED, (unsigned long long)c_issued);
+        }
+        c_comp = c_ab = c_cells = c_issued = 0;
+    };
+    // candidate rows (row, row+1) -> dst (2D values); row even; row+1 may be n
+    auto load_pair = [&](T (&dst)[2 * D], const T* cr, int row) {
+        if constexpr (VEC) {
+            if (row + 1 < n) {
+                const typename PL::V* src = reinterpret_cast<const typename PL::V*>(cr + (int64_t)row * D);
+#pragma unroll
+                for (int v = 0; v < PL::nv; ++v) {
+                    const typename PL::V x = __ldg(src + v);
+                    const T* xs = reinterpret_cast<const T*>(&x);
+#pragma unroll
+                    for (int u = 0; u < PL::per; ++u) dst[v * PL::per + u] = xs[u];
+                }
+                return;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2 * D; ++u) dst[u] = (row + u / D < n) ? __ldg(cr + (int64_t)row * D + u) : T(0);
+    };
+    auto load_col = [&](T (&dst)[D], int col) {  // query column (INF past the end)
+        if (col < n) {
+            if constexpr (QV) {
+                const T2* s2 = reinterpret_cast<const T2*>(qser + (int64_t)col * D);
+#pragma unroll
+                for (int pp = 0; pp < DP; ++pp) {
+                    const T2 v = __ldg(s2 + pp);
+                    dst[2 * pp] = v.x;
+                    dst[2 * pp + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < D; ++p) dst[p] = __ldg(qser + (int64_t)col * D + p);
+            }
+        } else {
+#pragma unroll
+            for (int p = 0; p < D; ++p) dst[p] = INF;
+        }
+    };
+    auto put_col = [&](int slot, const T (&src)[D]) {
+        T2* dst = ring + slot * DP * 32;
+#pragma unroll
+        for (int pp = 0; pp < DP; ++pp) dst[pp * 32] = T2{src[2 * pp], (2 * pp + 1 < D) ? src[2 * pp + 1] : T(0)};
+    };
+    auto load_env = [&](T (&uv)[D], T (&lv)[D], int row) {  // envelope row of the lane's query
+        const T* eu = a.env_up + ((int64_t)q * n + row) * D;
+        const T* el = a.env_lo + ((int64_t)q * n + row) * D;
+        if constexpr (QV) {
+#pragma unroll
+            for (int pp = 0; pp < DP; ++pp) {
+                const T2 x = __ldg(reinterpret_cast<const T2*>(eu) + pp);
+                const T2 y = __ldg(reinterpret_cast<const T2*>(el) + pp);
+                uv[2 * pp] = x.x; uv[2 * pp + 1] = x.y;
+                lv[2 * pp] = y.x; lv[2 * pp + 1] = y.y;
+            }
+        } else {
+#pragma unroll
+            for (int p = 0; p < D; ++p) {
+                uv[p] = __ldg(eu + p);
+                lv[p] = __ldg(el + p);
+            }
+        }
+    };
+    auto lb_term = [&](const T (&c)[D], const T (&uv)[D], const T (&lv)[D]) -> T {  // LB_MV term of one row
+        T t2 = T(0);
+#pragma unroll
+        for (int p = 0; p < D; ++p) {
+            const T dv = tmax(tmax(c[p] - uv[p], lv[p] - c[p]), T(0));
+            t2 = fma(dv, dv, t2);
+        }
+        return fast_sqrt(t2);
+    };
+    // refill free lanes; a new pair starts with `prev` as its row -1 band
+    auto refill = [&](T (&prev)[B]) {
+        unsigned freem = __ballot_sync(FULL, !busy);
+        while (freem && !exhausted) {
+            if (t_next >= t_len) {
+                int64_t tile = 0;
+                if (lane == 0) tile = atomicAdd(tile_ctr, 1);
+                tile = __shfl_sync(FULL, tile, 0);
+                if (tile >= n_tiles) {
+                    exhausted = true;
+                    break;
+                }
+                t_q = (int)tl.q[tile];
+                t_begin = tl.begin[tile];
+                t_len = tl.len[tile];
+                t_next = 0;
+                // prefetch the tile: lane m holds entry m's candidate, bound,
+                // state and first two candidate rows
+                if (lane < t_len) {
+                    const int64_t e = t_begin + lane;
+                    pf_c = cand_of[e];
+                    pf_res = res[e];
+                    pf_lb = casc ? a.lb[(int64_t)t_q * a.N + pf_c] : T(0);
+                    load_pair(pf_pair, a.cands + (int64_t)pf_c * n * D, 0);
+                }
+                t_thr_raw = a.abandon ? load_volatile(a.dbest + t_q) : INF;
+                if (t_q != staged_q) {
+                    __syncwarp();
+                    const T* qs = a.queries + (int64_t)t_q * n * D;
+                    for (int e = lane; e < (W + 1) * DP; e += 32) {
+                        const int col = e / DP, pp = e - (e / DP) * DP;
+                        qstage[e] = (col < n) ? T2{__ldg(qs + col * D + 2 * pp),
+                                                   (2 * pp + 1 < D) ? __ldg(qs + col * D + 2 * pp + 1) : T(0)}
+                                              : T2{INF, INF};
+                    }
+                    staged_q = t_q;
+                    __syncwarp();
+                }
+            }
+            const int take = min(t_len - t_next, __popc(freem));
+            const int rank = __popc(freem & ((1u << lane) - 1u));
+            const int m = t_next + (rank < take ? rank : 0);  // tile position this lane would take
+            const uint32_t c_m = __shfl_sync(FULL, pf_c, m);
+            const T lb_m = __shfl_sync(FULL, pf_lb, m);
+            const T res_m = __shfl_sync(FULL, pf_res, m);
+            T pr_m[2 * D];
+#pragma unroll
+            for (int u = 0; u < 2 * D; ++u) pr_m[u] = __shfl_sync(FULL, pf_pair[u], m);
+            if (!busy && rank < take && !(res_m < T(0))) {  // skip entries pruned by the advanced bound
+                if (t_q != cq) {
+                    flush();
+                    cq = t_q;
+                }
+                q = t_q;
+                ent = t_begin + m;
+                crow = a.cands + (int64_t)c_m * n * D;
+                qser = a.queries + (int64_t)q * n * D;
+                lbtot = lb_m;
+                prefix = T(0);
+                thr = a.abandon ? scale_up<T>(t_thr_raw, a.mg.prune) : INF;
+                thr_pend_raw = t_thr_raw;
+#pragma unroll
+                for (int k = 0; k < B; ++k) prev[k] = (k == W) ? T(0) : INF;
+                // ring: column k-W in slot k (INF for k < W), from the staged copy
+#pragma unroll
+                for (int k = 0; k < W; ++k)
+#pragma unroll
+                    for (int pp = 0; pp < DP; ++pp) ring[(k * DP + pp) * 32] = T2{INF, INF};
+#pragma unroll
+                for (int k = W; k < B; ++k)
+#pragma unroll
+                    for (int pp = 0; pp < DP; ++pp) ring[(k * DP + pp) * 32] = qstage[(k - W) * DP + pp];
+                load_col(x1, W + 1);
+                load_col(x2, W + 2);
+                if (casc) {
+                    load_env(eu0, el0, 0);
+                    load_env(eu1, el1, 1 < n ? 1 : 0);
+                }
+#pragma unroll
+                for (int p = 0; p < D; ++p) {
+                    c0[p] = pr_m[p];
+                    c1[p] = pr_m[D + p];
+                }
+                T nx[2 * D];
+                load_pair(nx, crow, 2);
+#pragma unroll
+                for (int p = 0; p < D; ++p) {
+                    n0[p] = nx[p];
+                    n1[p] = nx[D + p];
+                }
+                i = 0;
+                h = 0;
+                since = 0;
+                busy = true;
+            }
+            t_next += take;
+            freem = __ballot_sync(FULL, !busy);
+        }
+    };
+    // two rows (i, i+1): P = row i-1 band in, row i out; N = row i+1 out
+    auto step = [&](T (&P)[B], T (&N)[B]) {
+        const bool two = (i + 1 < n);
+        T rmin0, rmin1;
+        dtw_step2<T, D, B, EXACT>(P, N, c0, c1, ring, h, x1, rmin0, rmin1);
+        // cascade terms of rows i, i+1 from envelope rows loaded a step ago
+        T suf0 = T(0), suf1 = T(0);
+        if (casc) {
+            prefix += lb_term(c0, eu0, el0);
+            suf0 = tmax(lbtot * a.casc_lo - prefix * a.casc_hi, T(0));
+            if (two) {
+                prefix += lb_term(c1, eu1, el1);
+                suf1 = tmax(lbtot * a.casc_lo - prefix * a.casc_hi, T(0));
+            }
+        }
+        const T bound0 = rmin0 + suf0, bound1 = rmin1 + suf1;
+        int stop = -1;
+        bool abandoned = false;
+        T fin = INF;
+        if (rmin0 > thr || bound0 > thr * a.casc_thr) {
+            stop = i;
+            abandoned = true;
+        } else if (!two) {  // row i is the last row
+            stop = i;
+#pragma unroll
+            for (int k = 0; k < B; ++k)
+                if (k == W) fin = P[k];
+            abandoned = fin > thr;  // dtw.py:101-102
+        } else if (rmin1 > thr || bound1 > thr * a.casc_thr) {
+            stop = i + 1;
+            abandoned = true;
+        } else if (i + 1 == n - 1) {
+            stop = i + 1;
+#pragma unroll
+            for (int k = 0; k < B; ++k)
+                if (k == W) fin = N[k];
+            abandoned = fin > thr;
+        }
+        if (stop >= 0) {
+            res[ent] = abandoned ? INF : fin;
+            if (!abandoned) atomic_min_nonneg<T>(a.dbest + q, fin);
+            ++c_comp;
+            c_ab += abandoned ? 1 : 0;
+            c_cells += cells_upto(stop, n, W);
+            busy = false;
+            return;
+        }
+        // slide two columns: i+W+1 -> slot of i-W (h), i+W+2 -> slot of i-W+1
+        put_col(h, x1);
+        put_col(h + 1 == B ? 0 : h + 1, x2);
+        i += 2;
+        h += 2;
+        h = h >= B ? h - B : h;
+#pragma unroll
+        for (int p = 0; p < D; ++p) {
+            c0[p] = n0[p];
+            c1[p] = n1[p];
+        }
+        if (i + 2 < n) {
+            T nx[2 * D];
+            load_pair(nx, crow, i + 2);
+#pragma unroll
+            for (int p = 0; p < D; ++p) {
+                n0[p] = nx[p];
+                n1[p] = nx[D + p];
+            }
+        }
+        // operands of the next step, consumed after its DP
+        load_col(x1, i + W + 1);
+        load_col(x2, i + W + 2);
+        if (casc) {
+            load_env(eu0, el0, i);
+            load_env(eu1, el1, i + 1 < n ? i + 1 : i);
+        }
+        since += 2;
+        if (since >= 8) {
+            // the best-so-far read issued 8 rows ago; issue the next one
+            since = 0;
+            thr = scale_up<T>(thr_pend_raw, a.mg.prune);
+            if (a.abandon) thr_pend_raw = load_volatile(a.dbest + q);
+        }
+    };
+    // One copy of the step keeps the body inside the 32 KB L1.5 I-cache;
+    // row i+1's band moves back into bandA (B register moves per two rows).
+    while (true) {
+        refill(bandA);
+        if (!__any_sync(FULL, busy) && exhausted) break;
+        c_issued += 2 * B;
+        if (busy) {
+            step(bandA, bandB);
+#pragma unroll
+            for (int k = 0; k < B; ++k) bandA[k] = bandB[k];
+        }
+    }
+    flush();
+}
+
+// (T, d, 2W+1) shapes served by dtw_lane_kernel; others use the lockstep
+// kernels below.  C0: (double,3,25); C1a: (float,5,25); C2: (float,20,13);
+// C4: (float,6,25).
+#define TCDTW_LANE_SPECS(X) \
+    X(float, 3, 25) X(float, 4, 25) X(float, 5, 25) X(float, 6, 25) X(float, 8, 25) \
+    X(float, 3, 13) X(float, 5, 13) X(float, 6, 13) X(float, 8, 13) X(double, 3, 25)
+
+template <typename T>
+static int launch_lane(const SArgs<T>& a, int d, int B, Tiles tl, int64_t n_tiles, const uint32_t* cand_of, T* res,
+                       int* tctr, cudaStream_t st) {
+    constexpr int threads = 64;
+    auto go = [&](auto kern, int DD, int BB) -> int {
+        int dev = 0, sms = 148, occ = 1;
+        const size_t smem = (size_t)(threads / 32) * ((size_t)BB * ((DD + 1) / 2) * 32 + (size_t)(BB / 2 + 1) * ((DD + 1) / 2)) * 2 * sizeof(T);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (smem > 227 * 1024) return TCDTW_NOT_SUPPORTED;
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return TCDTW_NOT_SUPPORTED;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        if (occ < 1) return TCDTW_NOT_SUPPORTED;
+        int64_t grid = (int64_t)occ * sms;
+        const int64_t need = (n_tiles + 1) / 2;
+        if (grid > need) grid = need;
+        cudaMemsetAsync(tctr, 0, sizeof(int), st);
+        kern<<<(int)grid, threads, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
+        return launch_status();
+    };
+    // 16-byte candidate-row blocks need aligned rows and whole blocks
+    const bool base_ok = (reinterpret_cast<uintptr_t>(a.cands) % 16) == 0;
+#define TCDTW_LANE_CASE(TT, DD, BB)                                                                      \
+    if constexpr (std::is_same<T, TT>::value) {                                                          \
+        if (d == DD && B == BB) {                                                                        \
+            constexpr size_t VB = sizeof(typename PairLoad<TT, DD>::V);                                  \
+            const bool vec = base_ok && (((int64_t)a.n * DD * sizeof(TT)) % VB) == 0;                    \
+            if (vec) return go(dtw_lane_kernel<TT, DD, BB, sizeof(TT) == 8, true>, DD, BB);              \
+            return go(dtw_lane_kernel<TT, DD, BB, sizeof(TT) == 8, false>, DD, BB);                      \
+        }                                                                                                \
+    }
+    TCDTW_LANE_SPECS(TCDTW_LANE_CASE)
+#undef TCDTW_LANE_CASE
+    return TCDTW_NOT_SUPPORTED;
+}
+
+// ------------------------------- DTW, warp per pair, anti-diagonal wavefront
+// Lane l owns row i0+l of a 32-row chunk and visits its band slot k at step
+// tau = k + 2l, so the cell above (slot k+1 of row i-1) arrives from lane
+// l-1 by one shuffle at tau-1 and the diagonal cell (slot k) at tau-2.  The
+// chunk's last row is handed to the next chunk through shared memory.
+// Abandoning (row min > thr) is evaluated per chunk with the first failing
+// row selected, which gives the reference's row-granular result.
+template <typename T, int DMAX, bool EXACT>
+__global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
+                                                       const uint32_t* __restrict__ cand_of, T* __restrict__ res,
+                                                       int* __restrict__ tile_ctr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int n = a.n, d = a.d, w = a.w, B = 2 * w + 1;
+    const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* qs = reinterpret_cast<T*>(smem_raw);                   // (n + 2w) * d
+    T* prow = qs + (size_t)(n + 2 * w) * d + (size_t)wib * B;  // per warp: B
+    __shared__ int64_t tile_s;
+    const T INF = dev_inf<T>();
+    int64_t cached_q = -1;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1);
+        __syncthreads();
+        const int64_t tile = tile_s;
+        if (tile >= n_tiles) break;
+        const int64_t q = tl.q[tile];
+        const int64_t e0 = tl.begin[tile];
+        const int len = tl.len[tile];
+        if (q != cached_q) {
+            const T* qsrc = a.queries + q * (int64_t)n * d;
+            for (int e = threadIdx.x; e < (n + 2 * w) * d; e += blockDim.x) {
+                const int r = e / d, p = e - (e / d) * d;
+                const int j = r - w;
+                qs[e] = (j >= 0 && j < n) ? qsrc[(int64_t)j * d + p] : INF;
+            }
+            cached_q = q;
+            __syncthreads();
+        }
+        for (int slot = wib; slot < len; slot += warps) {
+            const int64_t ent = e0 + slot;
+            if (res[ent] < T(0)) continue;  // pruned by the advanced bound (warp-uniform)
+            const int64_t c = cand_of[ent];
+            const T* crow = a.cands + c * (int64_t)n * d;
+            for (int k = lane; k < B; k += 32) prow[k] = (k == w) ? T(0) : INF;
+            __syncwarp();
+            T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg.prune) : INF;
+            T fin = INF;
+            bool abandoned = false;
+            int stop_row = n - 1;
+            for (int i0 = 0; i0 < n; i0 += 32) {
+                const int i = i0 + lane;
+                const bool valid = i < n;
+                T rp[DMAX];
+                load_point<T, DMAX>(rp, crow + (int64_t)(valid ? i : 0) * d, d);
+                T mine = INF, got = INF, rmin = INF;
+                const int steps = B + 62;
+                for (int tau = 0; tau < steps; ++tau) {
+                    const int k = tau - 2 * lane;
+                    const T got_prev = got;
+                    got = __shfl_up_sync(0xffffffffu, mine, 1);
+                    const bool act = valid && k >= 0 && k < B;
+                    T v = INF;
+                    if (act) {
+                        T up, dg;
+                        if (lane == 0) {
+                            up = (k + 1 < B) ? prow[k + 1] : INF;
+                            dg = prow[k];
+                        } else {
+                            up = got;
+                            dg = got_prev;
+                        }
+                        const T* qp = qs + (size_t)(i + k) * d;
+                        T cost;
+                        if constexpr (EXACT) {
+                            cost = dist_exact<T, DMAX>(rp, qp, d);
+                        } else {
+                            T s = T(0);
+#pragma unroll
+                            for (int p = 0; p < DMAX; ++p)
+                                if (p < d) {
+                                    const T df = rp[p] - qp[p];
+                                    s = fma(df, df, s);
+                                }
+                            cost = fast_sqrt(s);
+                        }
+                        const T best = tmin(tmin(up, dg), mine);
+                        v = EXACT ? add_rn(cost, best) : cost + best;
+                        rmin = tmin(rmin, v);
+                        if (i == n - 1 && k == w) fin = v;
+                    }
+                    mine = v;
+                    __syncwarp();
+                    if (act && (lane == 31 || i == n - 1)) prow[k] = v;
+                    __syncwarp();
+                }
+                const unsigned bad = __ballot_sync(0xffffffffu, valid && rmin > thr);
+                if (bad) {
+                    const int first = __ffs(bad) - 1;
+                    abandoned = true;
+                    stop_row = i0 + first;
+                    break;
+                }
+                if (a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg.prune);
+            }
+            fin = __shfl_sync(0xffffffffu, fin, (n - 1) & 31);
+            if (!abandoned && fin > thr) abandoned = true;  // dtw.py:101-102
+            if (lane == 0) {
+                res[ent] = abandoned ? INF : fin;
+                if (!abandoned) atomic_min_nonneg<T>(a.dbest + q, fin);
+                int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
+                atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_DTW_COMPUTED), 1ull);
+                if (abandoned) atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_ABANDON_COUNT), 1ull);
+                atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_DTW_CELLS),
+                          (unsigned long long)cells_upto(stop_row, n, w));
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ------------------------------------------------- advanced bounds (step 2)
+// One lane per survivor, the tile's query shared by the warp; evaluated only
+// in the trigger band LB_MV > e * d_best (search.py:147).  A survivor whose
+// second bound exceeds thr is marked pruned (res = -1).
+template <typename T, int DMAX, bool EXACT>
+__global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
+                                                       const uint32_t* __restrict__ cand_of, T* __restrict__ res,
+                                                       T* __restrict__ ti_scratch, int* __restrict__ tile_ctr) {
+    const int n = a.n, d = a.d, w = a.w, B = 2 * w + 1;
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const T INF = dev_inf<T>();
+    while (true) {
+        int64_t tile = 0;
+        if (lane == 0) tile = atomicAdd(tile_ctr, 1);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile >= n_tiles) break;
+        const int64_t q = tl.q[tile];
+        const int64_t ent = tl.begin[tile] + lane;
+        const bool has = lane < tl.len[tile];
+        const int64_t c = has ? (int64_t)cand_of[ent] : 0;
+        const T db = load_volatile(a.dbest + q);
+        const T thr = scale_up<T>(db, a.mg.prune);
+        const T lb1 = has ? a.lb[q * a.N + c] : T(0);
+        // trigger band: b1 > e * d_best (search.py:147); EXACT uses the
+        // reference's float64 product
+        bool go = has && (EXACT ? ((double)lb1 > (double)a.trigger * (double)db)
+                                : (lb1 > a.trigger * db));
+        const T* qa = a.queries + q * (int64_t)n * d;
+        const T* ca = a.cands + c * (int64_t)n * d;
+        T val = T(0);
+        if (a.adv == TCDTW_METHOD_LB_PC) {
+            const T* bl = a.box_lo + q * (int64_t)a.G * a.K * d;
+            const T* bh = a.box_hi + q * (int64_t)a.G * a.K * d;
+            for (int t = 0; t < n && __any_sync(0xffffffffu, go && val <= thr); ++t) {
+                T cp[DMAX];
+                load_point<T, DMAX>(cp, ca + (int64_t)t * d, d);
+                const int g = t / a.gw;
+                T best = INF;
+                for (int k = 0; k < a.K; ++k) {
+                    const T* lo = bl + ((int64_t)g * a.K + k) * d;
+                    const T* hi = bh + ((int64_t)g * a.K + k) * d;
+                    T v2;
+                    if constexpr (EXACT) {
+                        v2 = boxdist2_exact<T, DMAX>(cp, lo, hi, d);
+                    } else {
+                        v2 = T(0);
+#pragma unroll
+                        for (int p = 0; p < DMAX; ++p)
+                            if (p < d) {
+                                const T dv = tmax(tmax(lo[p] - cp[p], cp[p] - hi[p]), T(0));
+                                v2 = fma(dv, dv, v2);
+                            }
+                    }
+                    best = tmin(best, v2);
+                }
+                val = EXACT ? add_rn(val, sqrt_rn(best)) : val + fast_sqrt(best);
+            }
+        } else if (a.adv == TCDTW_METHOD_LB_AD) {
+            for (int t = 0; t < n && __any_sync(0xffffffffu, go && val <= thr); ++t) {
+                T cp[DMAX];
+                load_point<T, DMAX>(cp, ca + (int64_t)t * d, d);
+                const int lo = t - w < 0 ? 0 : t - w;
+                const int hi = t + w > n - 1 ? n - 1 : t + w;
+                T m = INF;
+                for (int j = lo; j <= hi; ++j) {
+                    T dj;
+                    if constexpr (EXACT) {
+                        dj = dist_exact<T, DMAX>(cp, qa + (int64_t)j * d, d);
+                    } else {
+                        T s = T(0);
+#pragma unroll
+                        for (int p = 0; p < DMAX; ++p)
+                            if (p < d) {
+                                const T df = cp[p] - qa[(int64_t)j * d + p];
+                                s = fma(df, df, s);
+                            }
+                        dj = fast_sqrt(s);
+                    }
+                    m = tmin(m, dj);
+                }
+                val = EXACT ? add_rn(val, m) : val + m;
+            }
+        } else {
+            // LB_TI, TIP_TOP variant (search.py:150-153), lb_ti.py:140-200.
+            // Slot rings of size B per lane, interleaved by lane in scratch.
+            T* lo_r = ti_scratch + gwarp * 3 * (int64_t)B * 32;
+            T* up_r = lo_r + (int64_t)B * 32;
+            T* cm_r = up_r + (int64_t)B * 32;
+            const T* qst = a.qsteps + q * (int64_t)(n - 1);
+            T q0[DMAX];
+            load_point<T, DMAX>(q0, qa, d);
+            int hi = w < n - 1 ? w : n - 1;
+            if (go) {
+                for (int j = 0; j <= hi; ++j) {
+                    T cp[DMAX];
+                    load_point<T, DMAX>(cp, ca + (int64_t)j * d, d);
+                    T dd;
+                    if constexpr (EXACT) dd = dist_exact<T, DMAX>(cp, qa, d);
+                    else {
+                        T s = T(0);
+#pragma unroll
+                        for (int p = 0; p < DMAX; ++p) if (p < d) { const T df = cp[p] - q0[p]; s = fma(df, df, s); }
+                        dd = fast_sqrt(s);
+                    }
+                    const int r = j % B;
+                    lo_r[r * 32 + lane] = dd;
+                    up_r[r * 32 + lane] = dd;
+                    cm_r[r * 32 + lane] = dd;
+                }
+            }
+            int next_final = 0, prev_lo = 0, prev_hi = hi;
+            bool stop = !go;
+            for (int i = 1; i < n && __any_sync(0xffffffffu, !stop); ++i) {
+                const int lo = i - w > 0 ? i - w : 0;
+                hi = i + w < n - 1 ? i + w : n - 1;
+                if (!stop) {
+                    T qi[DMAX];
+                    load_point<T, DMAX>(qi, qa + (int64_t)i * d, d);
+                    auto pdist = [&](int j) -> T {
+                        T cp[DMAX];
+                        load_point<T, DMAX>(cp, ca + (int64_t)j * d, d);
+                        if constexpr (EXACT) return dist_exact<T, DMAX>(cp, qa + (int64_t)i * d, d);
+                        T s = T(0);
+#pragma unroll
+                        for (int p = 0; p < DMAX; ++p) if (p < d) { const T df = cp[p] - qi[p]; s = fma(df, df, s); }
+                        return fast_sqrt(s);
+                    };
+                    if (hi > prev_hi) cm_r[(hi % B) * 32 + lane] = INF;  // a new column enters
+                    if (i % a.period == 0) {
+                        for (int j = lo; j <= hi; ++j) {
+                            const T dd = pdist(j);
+                            const int r = j % B;
+                            lo_r[r * 32 + lane] = dd;
+                            up_r[r * 32 + lane] = dd;
+                        }
+                    } else {
+                        const T s = qst[i - 1];
+                        if (s > T(0))
+                            for (int j = prev_lo; j <= prev_hi; ++j) {
+                                const int r = j % B;
+                                T l = lo_r[r * 32 + lane], u = up_r[r * 32 + lane];
+                                ti_advance<T>(l, u, s);
+                                lo_r[r * 32 + lane] = l;
+                                up_r[r * 32 + lane] = u;
+                            }
+                        if (hi > prev_hi) {
+                            const T dd = pdist(hi);
+                            const int r = hi % B;
+                            lo_r[r * 32 + lane] = dd;
+                            up_r[r * 32 + lane] = dd;
+                        }
+                    }
+                    for (int j = lo; j <= hi; ++j) {
+                        const int r = j % B;
+                        const T l = lo_r[r * 32 + lane];
+                        if (l < cm_r[r * 32 + lane]) cm_r[r * 32 + lane] = l;
+                    }
+                    while (next_final <= i - w) {
+                        const T cmv = cm_r[(next_final % B) * 32 + lane];
+                        val = EXACT ? add_rn(val, cmv) : val + cmv;
+                        ++next_final;
+                        if (val > thr) { stop = true; break; }
+                    }
+                }
+                prev_lo = lo;
+                prev_hi = hi;
+            }
+            if (!stop) {
+                while (next_final < n) {
+                    const T cmv = cm_r[(next_final % B) * 32 + lane];
+                    val = EXACT ? add_rn(val, cmv) : val + cmv;
+                    ++next_final;
+                }
+            }
+        }
+        if (go && val > thr) res[ent] = T(-1);
+        int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
+        warp_add_counter(ctr + TCDTW_C_ADVANCED_LB_EVALS, go ? 1 : 0);
+    }
+}
+
+// --------------------------------------------------------------- finalize
+// F1: per query minimum of completed DTWs (seeds and survivors).
+template <typename T>
+__global__ void fin_min_kernel(Tiles tl, int64_t n_tiles, const T* __restrict__ res, T* __restrict__ minv) {
+    for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
+         tile += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const int lane = threadIdx.x & 31;
+        const int64_t q = tl.q[tile];
+        T v = dev_inf<T>();
+        if (lane < tl.len[tile]) {
+            const T r = res[tl.begin[tile] + lane];
+            if (r >= T(0)) v = r;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = tmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0 && v < dev_inf<T>()) atomic_min_nonneg<T>(minv + q, v);
+    }
+}
+
+// EXACT float64 DTW of one pair by one thread; band rows in `scratch`
+// (2 * (2w+1) doubles).  Same arithmetic as dtw_pairs_kernel.
+template <int DMAX, typename TIn>
+__device__ double dtw_exact_thread(const TIn* qa, const TIn* ca, int n, int d, int w, double* scratch) {
+    const int width = 2 * w + 1;
+    double* prev = scratch;
+    double* cur = scratch + width;
+    const double INF = dev_inf<double>();
+    for (int k = 0; k < width; ++k) prev[k] = INF;
+    for (int i = 0; i < n; ++i) {
+        const int lo = i < w ? 0 : i - w;
+        const int hi = i + w >= n ? n - 1 : i + w;
+        for (int k = 0; k < width; ++k) cur[k] = INF;
+        double qi[DMAX];
+#pragma unroll
+        for (int p = 0; p < DMAX; ++p) qi[p] = p < d ? (double)qa[(int64_t)i * d + p] : 0.0;
+        int k = lo - i + w;
+        for (int j = lo; j <= hi; ++j, ++k) {
+            double sq[DMAX];
+#pragma unroll
+            for (int p = 0; p < DMAX; ++p) {
+                if (p < d) {
+                    const double df = __dsub_rn(qi[p], (double)ca[(int64_t)j * d + p]);
+                    sq[p] = __dmul_rn(df, df);
+                } else {
+                    sq[p] = 0.0;
+                }
+            }
+            const double cost = __dsqrt_rn(np_sum<double, DMAX>(sq, d));
+            double v;
+            if (i == 0 && j == 0) {
+                v = cost;
+            } else {
+                double best = INF;
+                if (i > 0) {
+                    if (k + 1 < width) best = prev[k + 1];
+                    if (j > 0 && prev[k] < best) best = prev[k];
+                }
+                if (k > 0 && cur[k - 1] < best) best = cur[k - 1];
+                v = __dadd_rn(cost, best);
+            }
+            cur[k] = v;
+        }
+        double* t = prev;
+        prev = cur;
+        cur = t;
+    }
+    return prev[w];
+}
+
+// F2/F3 (FAST): finalists (float32 DTW within the margin of the best) are
+// re-scored in float64; pass 0 takes the minimum, pass 1 the lowest index
+// attaining it.  EXACT: pass 1 only, on the stored exact values.
+template <typename T, int DMAX>
+__global__ void fin_rescore_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles, const uint32_t* __restrict__ cand_of,
+                                   const T* __restrict__ res, const T* __restrict__ minv, const T* __restrict__ dbest_in,
+                                   int pass, unsigned long long* __restrict__ min64,
+                                   unsigned long long* __restrict__ best_idx, double* __restrict__ scratch) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gthread = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int width = 2 * a.w + 1;
+    double* my_scratch = scratch + gthread * 2 * (int64_t)width;
+    for (int64_t tile = gthread >> 5; tile < n_tiles; tile += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t q = tl.q[tile];
+        const bool has = lane < tl.len[tile];
+        const int64_t ent = tl.begin[tile] + lane;
+        if (!has) continue;
+        const T r = res[ent];
+        if (!(r >= T(0)) || r == dev_inf<T>()) continue;
+        const uint32_t c = cand_of[ent];
+        if constexpr (sizeof(T) == 8) {
+            // EXACT: stored values are the reference's
+            if (r == minv[q]) atomicMin(best_idx + q, (unsigned long long)c);
+        } else {
+            T bound = minv[q];
+            if (dbest_in) bound = tmin(bound, dbest_in[q]);
+            const T thr = __fmul_ru(bound, a.mg.fin);
+            if (!(r <= thr)) continue;
+            const double d64 = dtw_exact_thread<DMAX, T>(a.queries + q * (int64_t)a.n * a.d,
+                                                        a.cands + (int64_t)c * a.n * a.d, a.n, a.d, a.w,
+                                                        my_scratch);
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(d64);
+            if (pass == 0) {
+                atomicMin(min64 + q, bits);
+                atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + q * TCDTW_COUNTERS + TCDTW_C_FINALISTS),
+                          1ull);
+            } else if (bits == min64[q]) {
+                atomicMin(best_idx + q, (unsigned long long)c);
+            }
+        }
+    }
+}
+
+template <typename T>
+__global__ void fin_output_kernel(int64_t Q, int64_t N, int64_t base, const T* __restrict__ minv,
+                                  const unsigned long long* __restrict__ min64,
+                                  const unsigned long long* __restrict__ best_idx, const int64_t* __restrict__ ctr,
+                                  int has_lb, int64_t* __restrict__ out_idx, double* __restrict__ out_dist,
+                                  int64_t* __restrict__ out_ctr) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < Q; q += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long bi = best_idx[q];
+        double dist;
+        if constexpr (sizeof(T) == 8) dist = (double)minv[q];
+        else dist = __longlong_as_double((long long)min64[q]);
+        if (bi == 0xffffffffffffffffull) {
+            out_idx[q] = -1;
+            out_dist[q] = dev_inf<double>();
+        } else {
+            out_idx[q] = (int64_t)bi + base;
+            out_dist[q] = dist;
+        }
+        const int64_t* c = ctr + q * TCDTW_COUNTERS;
+        int64_t* o = out_ctr ? out_ctr + q * TCDTW_COUNTERS : nullptr;
+        if (o) {
+            for (int k = 0; k < TCDTW_COUNTERS; ++k) o[k] = c[k];
+            o[TCDTW_C_DTW_SKIPPED] = N - c[TCDTW_C_DTW_COMPUTED];
+            o[TCDTW_C_LB_MV_EVALS] = has_lb ? N : 0;
+        }
+    }
+}
+
+template <typename T>
+__global__ void fill_kernel(T* p, int64_t n, T v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// ----------------------------------------------------------- ALU probe
+template <typename T>
+__global__ void alu_probe_kernel(int iters, T* sink) {
+    T a0 = T(threadIdx.x) * T(1e-7), a1 = a0 + T(1), a2 = a0 + T(2), a3 = a0 + T(3);
+    T a4 = a0 + T(4), a5 = a0 + T(5), a6 = a0 + T(6), a7 = a0 + T(7);
+    const T m = T(0.999999), c = T(1e-7);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+            a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+        }
+    }
+    if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == T(-1)) sink[0] = a0;
+}
+
+// =================================================================== plan
+struct Plan {
+    int64_t Q, N;
+    int n, d, w, B, G, K, S, n_chunks;
+    size_t es;  // element size
+    bool has_lb, exact;
+    int64_t max_tiles;
+    // byte offsets
+    size_t o_qT, o_ub;
+    size_t o_up, o_lo, o_upT, o_loT, o_candT, o_steps, o_blo, o_bhi, o_bcnt, o_lb, o_seed, o_seedres,
+        o_seedcnt, o_dbest, o_ccnt, o_coff, o_surv, o_res, o_tcnt, o_toff, o_tq, o_tb, o_tl, o_sq, o_sb, o_sl,
+        o_ctr, o_minv, o_min64, o_bidx, o_tctr, o_cub, o_fsc, o_tisc, total;
+    size_t cub_bytes;
+    int fin_threads, adv_warps;
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
+    if (!dsc) return TCDTW_INVALID_INPUT;
+    if (dsc->dtype != TCDTW_F32 && dsc->dtype != TCDTW_F64) return TCDTW_INVALID_INPUT;
+    if (dsc->n < 1 || dsc->dims < 1 || dsc->dims > kMaxDims || dsc->window < 0) return TCDTW_INVALID_INPUT;
+    if (dsc->n_queries < 1 || dsc->n_candidates < 1 || dsc->n_candidates > 0xfffffff0LL) return TCDTW_INVALID_INPUT;
+    if (dsc->method < TCDTW_METHOD_NONE || dsc->method > TCDTW_METHOD_LB_AD) return TCDTW_INVALID_INPUT;
+    if (dsc->refresh_period < 1 || dsc->quant_levels < 1 || dsc->max_boxes < 1 || dsc->group_width < 1)
+        return TCDTW_INVALID_INPUT;
+    if (!(dsc->trigger_ti > 0.0 && dsc->trigger_ti < 1.0) || !(dsc->trigger_pc > 0.0 && dsc->trigger_pc < 1.0))
+        return TCDTW_INVALID_INPUT;
+    if (!(dsc->min_cell_frac > 0.0)) return TCDTW_INVALID_INPUT;
+    if (dsc->method == TCDTW_METHOD_TC_DTW && dsc->advanced != TCDTW_METHOD_LB_TI &&
+        dsc->advanced != TCDTW_METHOD_LB_PC)
+        return TCDTW_INVALID_INPUT;  // search.py:64-66
+    Plan& p = *P;
+    p.Q = dsc->n_queries;
+    p.N = dsc->n_candidates;
+    p.n = dsc->n;
+    p.d = dsc->dims;
+    p.w = dsc->window < dsc->n - 1 ? dsc->window : dsc->n - 1;
+    p.B = 2 * p.w + 1;
+    p.G = (p.n - 1) / dsc->group_width + 1;
+    p.K = dsc->max_boxes;
+    p.exact = dsc->dtype == TCDTW_F64;
+    p.es = p.exact ? 8 : 4;
+    p.has_lb = dsc->method != TCDTW_METHOD_NONE;
+    p.S = p.has_lb ? (dsc->seeds > 0 ? dsc->seeds : 8) : 0;
+    if (p.S > kSeedMax) return TCDTW_INVALID_INPUT;
+    if (p.S > p.N) p.S = (int)p.N;
+    if (p.S > 0 && p.S != 1 && p.S != 2 && p.S != 4 && p.S != 8 && p.S != 16 && p.S != 32) {
+        int s = 1;
+        while (s < p.S) s <<= 1;
+        p.S = s > kSeedMax ? kSeedMax : s;
+    }
+    p.n_chunks = (int)((p.N + kChunk - 1) / kChunk);
+    p.max_tiles = p.Q * (p.N / kTile) + p.Q * (int64_t)p.n_chunks + p.Q;
+    const int64_t Q = p.Q, N = p.N;
+    const size_t es = p.es;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
+    const size_t series_q = (size_t)Q * p.n * p.d * es;
+    p.o_up = take(p.has_lb ? series_q : 0);
+    p.o_lo = take(p.has_lb ? series_q : 0);
+    p.o_upT = take(p.has_lb ? series_q : 0);
+    p.o_loT = take(p.has_lb ? series_q : 0);
+    p.o_qT = take(p.has_lb ? series_q : 0);
+    p.o_candT = take(p.has_lb ? (size_t)N * p.n * p.d * es : 0);
+    p.o_steps = take((size_t)Q * (p.n > 1 ? p.n - 1 : 1) * es);
+    const size_t boxes = (size_t)Q * p.G * p.K * p.d * es;
+    p.o_blo = take(boxes);
+    p.o_bhi = take(boxes);
+    p.o_bcnt = take((size_t)Q * p.G * 4);
+    p.o_lb = take(p.has_lb ? (size_t)Q * N * es : 0);
+    p.o_ub = take(p.has_lb ? (size_t)Q * N * es : 0);
+    p.o_seed = take((size_t)Q * kSeedMax * 4);
+    p.o_seedres = take((size_t)Q * kSeedMax * es);
+    p.o_seedcnt = take((size_t)Q * 4);
+    p.o_dbest = take((size_t)Q * es);
+    p.o_ccnt = take((size_t)Q * p.n_chunks * 8);
+    p.o_coff = take(((size_t)Q * p.n_chunks + 1) * 8);
+    p.o_surv = take((size_t)Q * N * 4);
+    p.o_res = take((size_t)Q * N * es);
+    p.o_tcnt = take(((size_t)Q * p.n_chunks + 1) * 8);
+    p.o_toff = take(((size_t)Q * p.n_chunks + 1) * 8);
+    p.o_tq = take((size_t)p.max_tiles * 4);
+    p.o_tb = take((size_t)p.max_tiles * 8);
+    p.o_tl = take((size_t)p.max_tiles * 4);
+    p.o_sq = take((size_t)Q * 4);
+    p.o_sb = take((size_t)Q * 8);
+    p.o_sl = take((size_t)Q * 4);
+    p.o_ctr = take((size_t)Q * TCDTW_COUNTERS * 8);
+    p.o_minv = take((size_t)Q * es);
+    p.o_min64 = take((size_t)Q * 8);
+    p.o_bidx = take((size_t)Q * 8);
+    p.o_tctr = take(16 * sizeof(int));
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b1, (int64_t*)nullptr, (int64_t*)nullptr, (int)(Q * p.n_chunks + 1));
+    b2 = b1;
+    p.cub_bytes = b1 > b2 ? b1 : b2;
+    p.o_cub = take(p.cub_bytes);
+    p.fin_threads = 148 * 256;
+    p.o_fsc = take((size_t)p.fin_threads * 2 * p.B * 8);
+    p.adv_warps = 148 * 16;
+    const bool ti = dsc->method == TCDTW_METHOD_LB_TI ||
+                    (dsc->method == TCDTW_METHOD_TC_DTW && dsc->advanced == TCDTW_METHOD_LB_TI);
+    p.o_tisc = take(ti ? (size_t)p.adv_warps * 32 * 3 * p.B * es : 0);
+    p.total = o;
+    return TCDTW_OK;
+}
+
+template <typename T>
+static inline T* at(void* ws, size_t off) { return reinterpret_cast<T*>(reinterpret_cast<char*>(ws) + off); }
+
+// Phase timer: CUDA events on the launching stream.
+struct PhaseTimer {
+    bool on;
+    cudaStream_t st;
+    cudaEvent_t ev[TCDTW_PHASES + 1];
+    int first, last;
+    float* out;
+    PhaseTimer(const tcdtw_search_desc* dsc, cudaStream_t s, int f, int l)
+        : on(dsc->phase_ms && (dsc->flags & TCDTW_FLAG_TIMING)), st(s), first(f), last(l), out(dsc->phase_ms) {
+        if (on)
+            for (int i = first; i <= last + 1; ++i) cudaEventCreate(&ev[i]);
+    }
+    void mark(int i) {
+        if (on) cudaEventRecord(ev[i], st);
+    }
+    void finish() {
+        if (!on) return;
+        cudaEventSynchronize(ev[last + 1]);
+        for (int i = first; i <= last; ++i) cudaEventElapsedTime(&out[i], ev[i], ev[i + 1]);
+        for (int i = first; i <= last + 1; ++i) cudaEventDestroy(ev[i]);
+    }
+};
+
+static int sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+#define TRY(x)                         \
+    do {                               \
+        int _s = (x);                  \
+        if (_s != TCDTW_OK) return _s; \
+    } while (0)
+
+// TCDTW_DEBUG=1: synchronise and report after every pipeline stage.
+static void dbg_stage(cudaStream_t st, const char* what) {
+    static const bool on = getenv("TCDTW_DEBUG") != nullptr;
+    if (!on) return;
+    cudaError_t e = cudaStreamSynchronize(st);
+    fprintf(stderr, "[tcdtw] %-24s %s\n", what, cudaGetErrorString(e));
+    fflush(stderr);
+}
+
+template <typename T>
+static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const void* queries, const void* cands,
+                          void* ws) {
+    SArgs<T> a;
+    a.queries = (const T*)queries;
+    a.cands = (const T*)cands;
+    a.lb = p.has_lb ? at<T>(ws, p.o_lb) : nullptr;
+    a.env_up = p.has_lb ? at<T>(ws, p.o_up) : nullptr;
+    a.env_lo = p.has_lb ? at<T>(ws, p.o_lo) : nullptr;
+    a.dbest = at<T>(ws, p.o_dbest);
+    a.box_lo = at<T>(ws, p.o_blo);
+    a.box_hi = at<T>(ws, p.o_bhi);
+    a.qsteps = at<T>(ws, p.o_steps);
+    a.counters = at<int64_t>(ws, p.o_ctr);
+    a.N = p.N;
+    a.n = p.n;
+    a.d = p.d;
+    a.w = p.w;
+    a.G = p.G;
+    a.K = p.K;
+    a.gw = dsc->group_width;
+    a.period = dsc->refresh_period;
+    a.method = dsc->method;
+    a.adv = -1;
+    if (dsc->method == TCDTW_METHOD_TC_DTW) a.adv = dsc->advanced;
+    else if (dsc->method == TCDTW_METHOD_LB_TI || dsc->method == TCDTW_METHOD_LB_PC || dsc->method == TCDTW_METHOD_LB_AD)
+        a.adv = dsc->method;
+    a.trigger = (float)(a.adv == TCDTW_METHOD_LB_PC ? dsc->trigger_pc : dsc->trigger_ti);
+    if (p.exact) {
+        a.mg.prune = 1.0f;
+        a.mg.fin = 1.0f;
+        // float64: the cascaded bound tolerates 4(n+d) ulps of both sums
+        double s = 4.0 * (p.n + p.d) * 1.1102230246251565e-16;  // * 2^-53
+        s = s < 9.094947017729282e-13 ? 9.094947017729282e-13 : s;  // >= 2^-40
+        a.casc_lo = (T)(1.0 - s);
+        a.casc_hi = (T)(1.0 + s);
+        a.casc_thr = (T)(1.0 + s);
+    } else {
+        const double eps = (2.0 * p.n + p.d + 16.0) * 1.1920928955078125e-07;  // * 2^-23
+        a.mg.prune = nextafterf((float)(1.0 + 3.0 * eps), 2.0f);
+        a.mg.fin = nextafterf((float)(1.0 + 2.5 * eps), 2.0f);
+        a.casc_lo = (T)(1.0 - eps);
+        a.casc_hi = (T)(1.0 + 2.0 * eps);
+        a.casc_thr = (T)1.0;  // thr already carries the (1+3 eps) margin
+    }
+    a.abandon = dsc->method != TCDTW_METHOD_NONE;
+    return a;
+}
+
+// DTW launcher over a tile list: thread-per-pair if the band fits the
+// register buckets, else the wavefront kernel.
+template <typename T, int DMAX, bool EXACT>
+static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tiles, const uint32_t* cand_of, T* res,
+                      int* tctr, cudaStream_t st) {
+    if (n_tiles <= 0) return TCDTW_OK;
+    static const bool no_lane = getenv("TCDTW_NO_LANE") != nullptr;  // A/B switch for benchmarking
+    if (!no_lane) {
+        const int s = launch_lane<T>(a, p.d, p.B, tl, n_tiles, cand_of, res, tctr, st);
+        if (s != TCDTW_NOT_SUPPORTED) return s;
+    }
+    cudaMemsetAsync(tctr, 0, sizeof(int), st);
+    const int sms = sm_count();
+    constexpr int VEC = 16 / sizeof(T);
+    const int DP = (p.d + VEC - 1) / VEC * VEC;
+    if (p.B <= 64) {
+        const size_t smem = (size_t)8 * (p.n + 2 * p.w) * DP * sizeof(T);
+        auto run = [&](auto kern) -> int {
+            if (smem > 48 * 1024 &&
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return TCDTW_NOT_SUPPORTED;
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+            if (occ < 1) return TCDTW_NOT_SUPPORTED;
+            int64_t grid = (int64_t)occ * sms;
+            const int64_t need = (n_tiles + 7) / 8;
+            if (grid > need) grid = need;
+            kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
+            return launch_status();
+        };
+        if (p.B <= 8) return run(dtw_tpp_kernel<T, DMAX, 8, EXACT>);
+        if (p.B <= 16) return run(dtw_tpp_kernel<T, DMAX, 16, EXACT>);
+        if (p.B <= 32) return run(dtw_tpp_kernel<T, DMAX, 32, EXACT>);
+        return run(dtw_tpp_kernel<T, DMAX, 64, EXACT>);
+    }
+    const size_t smem = ((size_t)(p.n + 2 * p.w) * p.d + (size_t)8 * p.B) * sizeof(T);
+    auto kern = dtw_wave_kernel<T, DMAX, EXACT>;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return TCDTW_NOT_SUPPORTED;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+    if (occ < 1) return TCDTW_NOT_SUPPORTED;
+    int64_t grid = (int64_t)occ * sms;
+    if (grid > n_tiles) grid = n_tiles;
+    kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
+    return launch_status();
+}
+
+template <typename T, int DMAX>
+struct SearchImpl {
+    static constexpr bool EXACT = sizeof(T) == 8;
+
+    static int seed(const tcdtw_search_desc* dsc, const Plan& p, const void* queries, const void* cands,
+                    const void* dr, void* ws, void* dbest_out, cudaStream_t st) {
+        PhaseTimer tm(dsc, st, 0, 3);
+        SArgs<T> a = make_args<T>(dsc, p, queries, cands, ws);
+        const int dtype = EXACT ? TCDTW_F64 : TCDTW_F32;
+        tm.mark(0);
+        cudaMemsetAsync(at<char>(ws, p.o_ctr), 0, (size_t)p.Q * TCDTW_COUNTERS * 8, st);
+        fill_kernel<T><<<grid_for(p.Q, 256), 256, 0, st>>>(a.dbest, p.Q, dev_inf<T>());
+        TRY(launch_status());
+        if (p.has_lb) {
+            TRY(series_envelope(dtype, queries, p.Q, p.n, p.d, p.w, at<T>(ws, p.o_up), at<T>(ws, p.o_lo), st));
+            TRY(planarize<T>(at<T>(ws, p.o_up), p.Q, p.n * p.d, at<T>(ws, p.o_upT), st));
+            TRY(planarize<T>(at<T>(ws, p.o_lo), p.Q, p.n * p.d, at<T>(ws, p.o_loT), st));
+            TRY(planarize<T>((const T*)queries, p.Q, p.n * p.d, at<T>(ws, p.o_qT), st));
+            TRY(planarize<T>((const T*)cands, p.N, p.n * p.d, at<T>(ws, p.o_candT), st));
+        }
+        if (a.adv == TCDTW_METHOD_LB_PC)
+            TRY(series_box_sets(dtype, queries, p.Q, p.n, p.d, p.w, dsc->group_width, dsc->quant_levels, p.K,
+                                dsc->min_cell_frac, dr, at<T>(ws, p.o_blo), at<T>(ws, p.o_bhi),
+                                at<int32_t>(ws, p.o_bcnt), st));
+        if (a.adv == TCDTW_METHOD_LB_TI && p.n > 1)
+            TRY(series_steps(dtype, queries, p.Q, p.n, p.d, at<T>(ws, p.o_steps), st));
+        dbg_stage(st, "prep");
+        tm.mark(1);
+        if (p.has_lb)
+            TRY((launch_lbmv_matrix<T, DMAX, EXACT>(at<T>(ws, p.o_upT), at<T>(ws, p.o_loT), at<T>(ws, p.o_qT),
+                                                    at<T>(ws, p.o_candT), p.Q, p.N, p.n, p.d, at<T>(ws, p.o_lb),
+                                                    at<T>(ws, p.o_ub), st)));
+        dbg_stage(st, "lb_mv");
+        tm.mark(2);
+        if (p.S > 0) {
+            uint32_t* seeds = at<uint32_t>(ws, p.o_seed);
+            int32_t* scnt = at<int32_t>(ws, p.o_seedcnt);
+            const int s_eff = (int)(p.S < p.N ? p.S : p.N);
+            switch (p.S) {
+                case 1: topk_kernel<T, 1><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
+                case 2: topk_kernel<T, 2><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
+                case 4: topk_kernel<T, 4><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
+                case 8: topk_kernel<T, 8><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
+                case 16: topk_kernel<T, 16><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
+                default: topk_kernel<T, 32><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
+            }
+            TRY(launch_status());
+            Tiles stl{at<uint32_t>(ws, p.o_sq), at<int64_t>(ws, p.o_sb), at<int32_t>(ws, p.o_sl)};
+            seed_tiles_kernel<<<grid_for(p.Q, 256), 256, 0, st>>>(p.Q, p.S, scnt, stl);
+            TRY(launch_status());
+            fill_kernel<T><<<grid_for(p.Q * p.S, 256), 256, 0, st>>>(at<T>(ws, p.o_seedres), p.Q * p.S, dev_inf<T>());
+            TRY(launch_status());
+            dbg_stage(st, "topk+tiles");
+            tm.mark(3);
+            TRY((launch_dtw<T, DMAX, EXACT>(a, p, stl, p.Q, seeds, at<T>(ws, p.o_seedres), at<int>(ws, p.o_tctr), st)));
+        } else {
+            tm.mark(3);
+        }
+        dbg_stage(st, "seed dtw");
+        tm.mark(4);
+        if (dbest_out && dbest_out != (void*)a.dbest)
+            cudaMemcpyAsync(dbest_out, a.dbest, (size_t)p.Q * sizeof(T), cudaMemcpyDeviceToDevice, st);
+        tm.finish();
+        return launch_status();
+    }
+
+    static int finish(const tcdtw_search_desc* dsc, const Plan& p, const void* queries, const void* cands,
+                      const void* dr, void* ws, const void* dbest_in, int64_t* best_index, double* best_distance,
+                      int64_t* counters, cudaStream_t st) {
+        (void)dr;
+        PhaseTimer tm(dsc, st, 4, 7);
+        SArgs<T> a = make_args<T>(dsc, p, queries, cands, ws);
+        const int sms = sm_count();
+        tm.mark(4);
+        if (dbest_in && dbest_in != (const void*)a.dbest)
+            cudaMemcpyAsync(a.dbest, dbest_in, (size_t)p.Q * sizeof(T), cudaMemcpyDeviceToDevice, st);
+        // compaction
+        const bool all = !p.has_lb;
+        int64_t* ccnt = at<int64_t>(ws, p.o_ccnt);
+        int64_t* coff = at<int64_t>(ws, p.o_coff);
+        dim3 cgrid((unsigned)p.n_chunks, (unsigned)p.Q);
+        if (p.Q > 65535) return TCDTW_INVALID_INPUT;
+        compact_count_kernel<T><<<cgrid, 256, 0, st>>>(a.lb, p.N, p.n_chunks, a.dbest, a.mg, all,
+                                                       at<uint32_t>(ws, p.o_seed), at<int32_t>(ws, p.o_seedcnt), p.S,
+                                                       ccnt);
+        TRY(launch_status());
+        cudaMemsetAsync(ccnt + p.Q * p.n_chunks, 0, 8, st);
+        size_t cb = p.cub_bytes;
+        if (cub::DeviceScan::ExclusiveSum(at<void>(ws, p.o_cub), cb, ccnt, coff, (int)(p.Q * p.n_chunks + 1), st) !=
+            cudaSuccess)
+            return TCDTW_CUDA_ERROR;
+        uint32_t* surv = at<uint32_t>(ws, p.o_surv);
+        T* res = at<T>(ws, p.o_res);
+        compact_write_kernel<T><<<cgrid, 256, 0, st>>>(a.lb, p.N, p.n_chunks, a.dbest, a.mg, all,
+                                                       at<uint32_t>(ws, p.o_seed), at<int32_t>(ws, p.o_seedcnt), p.S,
+                                                       coff, surv, res);
+        TRY(launch_status());
+        int64_t* tcnt = at<int64_t>(ws, p.o_tcnt);
+        int64_t* toff = at<int64_t>(ws, p.o_toff);
+        const int64_t n_seg = p.Q * p.n_chunks;
+        seg_tiles_count_kernel<<<grid_for(n_seg, 256), 256, 0, st>>>(p.Q, p.n_chunks, coff, tcnt, a.counters);
+        TRY(launch_status());
+        cudaMemsetAsync(tcnt + n_seg, 0, 8, st);
+        cb = p.cub_bytes;
+        if (cub::DeviceScan::ExclusiveSum(at<void>(ws, p.o_cub), cb, tcnt, toff, (int)(n_seg + 1), st) != cudaSuccess)
+            return TCDTW_CUDA_ERROR;
+        Tiles tl{at<uint32_t>(ws, p.o_tq), at<int64_t>(ws, p.o_tb), at<int32_t>(ws, p.o_tl)};
+        seg_tiles_fill_kernel<<<grid_for(n_seg, 128), 128, 0, st>>>(p.Q, p.n_chunks, coff, toff, tl);
+        TRY(launch_status());
+        // the number of tiles stays on the device: kernels stop at the first
+        // tile past the end (tile_q sentinel), bounded by max_tiles.
+        dbg_stage(st, "compact+tiles");
+        int64_t n_tiles = 0;
+        cudaMemcpyAsync(&n_tiles, toff + n_seg, 8, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        tm.mark(5);
+        if (a.adv >= 0 && n_tiles > 0) {
+            cudaMemsetAsync(at<int>(ws, p.o_tctr), 0, sizeof(int), st);
+            int grid = (p.adv_warps * 32) / 256;
+            advanced_kernel<T, DMAX, EXACT><<<grid, 256, 0, st>>>(a, tl, n_tiles, surv, res, at<T>(ws, p.o_tisc),
+                                                                 at<int>(ws, p.o_tctr));
+            TRY(launch_status());
+        }
+        dbg_stage(st, "advanced");
+        tm.mark(6);
+        TRY((launch_dtw<T, DMAX, EXACT>(a, p, tl, n_tiles, surv, res, at<int>(ws, p.o_tctr), st)));
+        dbg_stage(st, "dtw");
+        tm.mark(7);
+        // finalize
+        T* minv = at<T>(ws, p.o_minv);
+        unsigned long long* min64 = at<unsigned long long>(ws, p.o_min64);
+        unsigned long long* bidx = at<unsigned long long>(ws, p.o_bidx);
+        fill_kernel<T><<<grid_for(p.Q, 256), 256, 0, st>>>(minv, p.Q, dev_inf<T>());
+        TRY(launch_status());
+        cudaMemsetAsync(min64, 0x7f, (size_t)p.Q * 8, st);  // large positive sentinel
+        cudaMemsetAsync(bidx, 0xff, (size_t)p.Q * 8, st);
+        Tiles stl{at<uint32_t>(ws, p.o_sq), at<int64_t>(ws, p.o_sb), at<int32_t>(ws, p.o_sl)};
+        const uint32_t* seeds = at<uint32_t>(ws, p.o_seed);
+        const T* seedres = at<T>(ws, p.o_seedres);
+        const int fgrid = sms * 4;
+        if (p.S > 0) {
+            fin_min_kernel<T><<<fgrid, 256, 0, st>>>(stl, p.Q, seedres, minv);
+            TRY(launch_status());
+        }
+        if (n_tiles > 0) {
+            fin_min_kernel<T><<<fgrid, 256, 0, st>>>(tl, n_tiles, res, minv);
+            TRY(launch_status());
+        }
+        const T* dbi = (const T*)dbest_in;
+        double* fsc = at<double>(ws, p.o_fsc);
+        const int rgrid = p.fin_threads / 256;
+        for (int pass = EXACT ? 1 : 0; pass < 2; ++pass) {
+            if (p.S > 0) {
+                fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, stl, p.Q, seeds, seedres, minv, dbi, pass,
+                                                                   min64, bidx, fsc);
+                TRY(launch_status());
+            }
+            if (n_tiles > 0) {
+                fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, tl, n_tiles, surv, res, minv, dbi, pass, min64,
+                                                                   bidx, fsc);
+                TRY(launch_status());
+            }
+        }
+        fin_output_kernel<T><<<grid_for(p.Q, 256), 256, 0, st>>>(p.Q, p.N, dsc->candidate_base, minv, min64, bidx,
+                                                                a.counters, p.has_lb ? 1 : 0, best_index,
+                                                                best_distance, counters);
+        dbg_stage(st, "finalize");
+        tm.mark(8 > TCDTW_PHASES ? TCDTW_PHASES : 8);
+        tm.finish();
+        return launch_status();
+    }
+};
+
+struct SeedOp {
+    template <typename T, int DM>
+    int run(const tcdtw_search_desc* dsc, const Plan& p, const void* q, const void* c, const void* dr, void* ws,
+            void* dbo, cudaStream_t st) {
+        return SearchImpl<T, DM>::seed(dsc, p, q, c, dr, ws, dbo, st);
+    }
+};
+struct FinishOp {
+    template <typename T, int DM>
+    int run(const tcdtw_search_desc* dsc, const Plan& p, const void* q, const void* c, const void* dr, void* ws,
+            const void* dbi, int64_t* bi, double* bd, int64_t* ctr, cudaStream_t st) {
+        return SearchImpl<T, DM>::finish(dsc, p, q, c, dr, ws, dbi, bi, bd, ctr, st);
+    }
+};
+
+// Only the register buckets the search instantiates (d <= 32 covers C0-C4;
+// larger d goes through the 64/128 buckets).
+template <typename T, typename F, typename... Args>
+int dispatch_search_dims(int dims, F&& f, Args&&... args) {
+    if (dims <= 4) return f.template run<T, 4>(args...);
+    if (dims <= 8) return f.template run<T, 8>(args...);
+    if (dims <= 16) return f.template run<T, 16>(args...);
+    if (dims <= 32) return f.template run<T, 32>(args...);
+    return TCDTW_NOT_SUPPORTED;
+}
+
+}  // namespace tcdtw

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -m gpu -x > gpurun_out/t4.log 2>&1
+echo "pytest exit=$?" >> gpurun_out/t4.log
+timeout 900 python bench.py --steps 2 --warmup 1 --queries 1000 --method lb_mv --no-cpu-baseline > gpurun_out/bench4.log 2>&1
+echo "bench exit=$?" >> gpurun_out/bench4.log
