@@ -138,10 +138,42 @@ struct MvTile {
 };
 
 template <typename T, int DMAX, bool EXACT, bool UB>
+__device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT, const T* __restrict__ LT,
+                                                        const T* __restrict__ QTP, const T* __restrict__ CT_,
+                                                        int64_t Q, int64_t N, int n, int d, int TC,
+                                                        T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
+                                                        int64_t c0);
+
+template <typename T, int DMAX, bool EXACT, bool UB>
 __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ UT, const T* __restrict__ LT,
                                                           const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                           int64_t Q, int64_t N, int n, int d, int TC,
-                                                          T* __restrict__ out, T* __restrict__ ub_out) {
+                                                          T* __restrict__ out, T* __restrict__ ub_out, int ub_stride) {
+    using Tile = MvTile<T, DMAX, EXACT>;
+    constexpr int QT = Tile::QT, CTL = Tile::CT;
+    // query tiles vary fastest: concurrently resident blocks share one
+    // candidate tile, so each candidate byte leaves HBM once per batch and the
+    // (small) envelope tiles are re-read from L2.
+    const int64_t nqt = (Q + QT - 1) / QT;
+    const int64_t q0 = ((int64_t)blockIdx.x % nqt) * QT;
+    const int64_t c0 = ((int64_t)blockIdx.x / nqt) * CTL;
+    // the upper bound only seeds d_best: compute it on every ub_stride-th
+    // candidate tile (block-uniform)
+    if constexpr (UB) {
+        if (((int64_t)blockIdx.x / nqt) % ub_stride != 0) {
+            lbmv_matrix_kernel_body<T, DMAX, EXACT, false>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0);
+            return;
+        }
+    }
+    lbmv_matrix_kernel_body<T, DMAX, EXACT, UB>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0);
+}
+
+template <typename T, int DMAX, bool EXACT, bool UB>
+__device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT, const T* __restrict__ LT,
+                                                        const T* __restrict__ QTP, const T* __restrict__ CT_,
+                                                        int64_t Q, int64_t N, int n, int d, int TC,
+                                                        T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
+                                                        int64_t c0) {
     using Tile = MvTile<T, DMAX, EXACT>;
     constexpr int M = Tile::M, QT = Tile::QT, CTL = Tile::CT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -151,12 +183,6 @@ __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ 
     T* qs = cs + (size_t)TC * d * CTL;  // UB only
     const int tid = threadIdx.x;
     const int tq = tid & 15, tc = tid >> 4;
-    // query tiles vary fastest: concurrently resident blocks share one
-    // candidate tile, so each candidate byte leaves HBM once per batch and the
-    // (small) envelope tiles are re-read from L2.
-    const int64_t nqt = (Q + QT - 1) / QT;
-    const int64_t q0 = ((int64_t)blockIdx.x % nqt) * QT;
-    const int64_t c0 = ((int64_t)blockIdx.x / nqt) * CTL;
     T total[M][M], ubt[M][M];
 #pragma unroll
     for (int i = 0; i < M; ++i)
@@ -292,7 +318,7 @@ __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ 
 
 template <typename T, int DMAX, bool EXACT>
 int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int64_t Q, int64_t N, int n, int d,
-                       T* out, T* ub_out, cudaStream_t st) {
+                       T* out, T* ub_out, cudaStream_t st, int ub_stride = 1) {
     using Tile = MvTile<T, DMAX, EXACT>;
     const bool ub = ub_out != nullptr;
     const size_t per_t = (size_t)d * ((ub ? 3 : 2) * Tile::QT + Tile::CT) * sizeof(T);
@@ -309,14 +335,15 @@ int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int6
     const int64_t nct = (N + Tile::CT - 1) / Tile::CT;
     if (nqt * nct > 2147483647LL) return TCDTW_NOT_SUPPORTED;
     const unsigned grid = (unsigned)(nqt * nct);
-    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out);
+    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out, ub_stride);
     return launch_status();
 }
 
 // ------------------------------------------------------------ seeds (top-S)
 template <typename T, int S>
 __global__ void __launch_bounds__(256) topk_kernel(const T* __restrict__ lb, int64_t N, int s_eff, T* __restrict__ dbest,
-                                                   uint32_t* __restrict__ seeds, int32_t* __restrict__ seed_cnt) {
+                                                   uint32_t* __restrict__ seeds, int32_t* __restrict__ seed_cnt,
+                                                   int ct, int stride) {
     const int64_t q = blockIdx.x;
     const T* row = lb + q * N;
     T bv[S];
@@ -326,7 +353,10 @@ __global__ void __launch_bounds__(256) topk_kernel(const T* __restrict__ lb, int
         bv[k] = dev_inf<T>();
         bi[k] = 0xffffffffu;
     }
-    for (int64_t c = threadIdx.x; c < N; c += blockDim.x) {
+    // keys exist on every stride-th tile of ct candidates
+    for (int64_t k = threadIdx.x;; k += blockDim.x) {
+        const int64_t c = (k / ct) * ct * stride + (k % ct);
+        if (c >= N) break;
         const T v = row[c];
         if (v < bv[S - 1]) {
             bv[S - 1] = v;
@@ -527,7 +557,20 @@ struct SArgs {
     Margins mg;
     bool abandon;         // false for Method.NONE (search.py:135)
     T casc_lo, casc_hi, casc_thr;  // cascaded-abandon slack (see dtw_tpp_kernel)
+    // completed (not abandoned) DTWs, (q << 40 | entry), so the finalisation
+    // visits only them; nullptr for the seed pass
+    unsigned long long* done_list;
+    unsigned long long* done_cnt;
+    int64_t done_cap;
 };
+
+template <typename T>
+__device__ __forceinline__ void note_done(const SArgs<T>& a, int64_t q, int64_t ent) {
+    if (a.done_list) {
+        const unsigned long long k = atomicAdd(a.done_cnt, 1ull);
+        if ((int64_t)k < a.done_cap) a.done_list[k] = ((unsigned long long)q << 40) | (unsigned long long)ent;
+    }
+}
 
 __device__ __forceinline__ void warp_add_counter(int64_t* ctr, int64_t v) {
 #pragma unroll
@@ -672,6 +715,7 @@ __global__ void __launch_bounds__(256) dtw_tpp_kernel(SArgs<T> a, Tiles tl, int6
             stop_row = n - 1;
         }
         if (active) res[ent] = abandoned ? INF : fin;
+        if (active && !abandoned) note_done(a, q, ent);
         // best-so-far update and counters (warp-aggregated; one query per tile)
         T m = (active && !abandoned) ? fin : INF;
 #pragma unroll
@@ -1099,7 +1143,10 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
         }
         if (stop >= 0) {
             res[ent] = abandoned ? INF : fin;
-            if (!abandoned) atomic_min_nonneg<T>(a.dbest + q, fin);
+            if (!abandoned) {
+                atomic_min_nonneg<T>(a.dbest + q, fin);
+                note_done(a, q, ent);
+            }
             ++c_comp;
             c_ab += abandoned ? 1 : 0;
             c_cells += cells_upto(stop, n, W);
@@ -1309,7 +1356,10 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
             if (!abandoned && fin > thr) abandoned = true;  // dtw.py:101-102
             if (lane == 0) {
                 res[ent] = abandoned ? INF : fin;
-                if (!abandoned) atomic_min_nonneg<T>(a.dbest + q, fin);
+                if (!abandoned) {
+                    atomic_min_nonneg<T>(a.dbest + q, fin);
+                    note_done(a, q, ent);
+                }
                 int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
                 atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_DTW_COMPUTED), 1ull);
                 if (abandoned) atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_ABANDON_COUNT), 1ull);
@@ -1506,7 +1556,9 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
 // --------------------------------------------------------------- finalize
 // F1: per query minimum of completed DTWs (seeds and survivors).
 template <typename T>
-__global__ void fin_min_kernel(Tiles tl, int64_t n_tiles, const T* __restrict__ res, T* __restrict__ minv) {
+__global__ void fin_min_kernel(Tiles tl, int64_t n_tiles, const T* __restrict__ res, T* __restrict__ minv,
+                               const unsigned long long* __restrict__ done_cnt, int64_t done_cap) {
+    if (done_cnt && (int64_t)*done_cnt <= done_cap) return;  // the completed list covers it
     for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
          tile += (int64_t)gridDim.x * (blockDim.x >> 5)) {
         const int lane = threadIdx.x & 31;
@@ -1576,10 +1628,41 @@ __device__ double dtw_exact_thread(const TIn* qa, const TIn* ca, int n, int d, i
 // re-scored in float64; pass 0 takes the minimum, pass 1 the lowest index
 // attaining it.  EXACT: pass 1 only, on the stored exact values.
 template <typename T, int DMAX>
+__device__ __forceinline__ void rescore_entry(const SArgs<T>& a, int64_t q, int64_t ent,
+                                              const uint32_t* __restrict__ cand_of, const T* __restrict__ res,
+                                              const T* __restrict__ minv, const T* __restrict__ dbest_in, int pass,
+                                              unsigned long long* __restrict__ min64,
+                                              unsigned long long* __restrict__ best_idx, double* my_scratch) {
+    const T r = res[ent];
+    if (!(r >= T(0)) || r == dev_inf<T>()) return;
+    const uint32_t c = cand_of[ent];
+    if constexpr (sizeof(T) == 8) {
+        // EXACT: stored values are the reference's
+        if (r == minv[q]) atomicMin(best_idx + q, (unsigned long long)c);
+    } else {
+        T bound = minv[q];
+        if (dbest_in) bound = tmin(bound, dbest_in[q]);
+        const T thr = __fmul_ru(bound, a.mg.fin);
+        if (!(r <= thr)) return;
+        const double d64 = dtw_exact_thread<DMAX, T>(a.queries + q * (int64_t)a.n * a.d,
+                                                    a.cands + (int64_t)c * a.n * a.d, a.n, a.d, a.w, my_scratch);
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(d64);
+        if (pass == 0) {
+            atomicMin(min64 + q, bits);
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + q * TCDTW_COUNTERS + TCDTW_C_FINALISTS), 1ull);
+        } else if (bits == min64[q]) {
+            atomicMin(best_idx + q, (unsigned long long)c);
+        }
+    }
+}
+
+template <typename T, int DMAX>
 __global__ void fin_rescore_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles, const uint32_t* __restrict__ cand_of,
                                    const T* __restrict__ res, const T* __restrict__ minv, const T* __restrict__ dbest_in,
                                    int pass, unsigned long long* __restrict__ min64,
-                                   unsigned long long* __restrict__ best_idx, double* __restrict__ scratch) {
+                                   unsigned long long* __restrict__ best_idx, double* __restrict__ scratch,
+                                   const unsigned long long* __restrict__ done_cnt, int64_t done_cap) {
+    if (done_cnt && (int64_t)*done_cnt <= done_cap) return;  // the completed list covers it
     const int lane = threadIdx.x & 31;
     const int64_t gthread = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int width = 2 * a.w + 1;
@@ -1589,29 +1672,40 @@ __global__ void fin_rescore_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles, const 
         const bool has = lane < tl.len[tile];
         const int64_t ent = tl.begin[tile] + lane;
         if (!has) continue;
+        rescore_entry<T, DMAX>(a, q, ent, cand_of, res, minv, dbest_in, pass, min64, best_idx, my_scratch);
+    }
+}
+
+// The same over the completed list (q << 40 | entry), one thread per item.
+template <typename T>
+__global__ void fin_min_list_kernel(const unsigned long long* __restrict__ list,
+                                    const unsigned long long* __restrict__ done_cnt, int64_t done_cap,
+                                    const T* __restrict__ res, T* __restrict__ minv) {
+    const int64_t cnt = (int64_t)*done_cnt;
+    if (cnt > done_cap) return;  // overflowed: the tile kernels run instead
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < cnt; k += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long x = list[k];
+        const int64_t q = (int64_t)(x >> 40), ent = (int64_t)(x & ((1ull << 40) - 1));
         const T r = res[ent];
-        if (!(r >= T(0)) || r == dev_inf<T>()) continue;
-        const uint32_t c = cand_of[ent];
-        if constexpr (sizeof(T) == 8) {
-            // EXACT: stored values are the reference's
-            if (r == minv[q]) atomicMin(best_idx + q, (unsigned long long)c);
-        } else {
-            T bound = minv[q];
-            if (dbest_in) bound = tmin(bound, dbest_in[q]);
-            const T thr = __fmul_ru(bound, a.mg.fin);
-            if (!(r <= thr)) continue;
-            const double d64 = dtw_exact_thread<DMAX, T>(a.queries + q * (int64_t)a.n * a.d,
-                                                        a.cands + (int64_t)c * a.n * a.d, a.n, a.d, a.w,
-                                                        my_scratch);
-            const unsigned long long bits = (unsigned long long)__double_as_longlong(d64);
-            if (pass == 0) {
-                atomicMin(min64 + q, bits);
-                atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + q * TCDTW_COUNTERS + TCDTW_C_FINALISTS),
-                          1ull);
-            } else if (bits == min64[q]) {
-                atomicMin(best_idx + q, (unsigned long long)c);
-            }
-        }
+        if (r >= T(0) && r < dev_inf<T>()) atomic_min_nonneg<T>(minv + q, r);
+    }
+}
+
+template <typename T, int DMAX>
+__global__ void fin_rescore_list_kernel(SArgs<T> a, const unsigned long long* __restrict__ list,
+                                        const unsigned long long* __restrict__ done_cnt, int64_t done_cap,
+                                        const uint32_t* __restrict__ cand_of, const T* __restrict__ res,
+                                        const T* __restrict__ minv, const T* __restrict__ dbest_in, int pass,
+                                        unsigned long long* __restrict__ min64, unsigned long long* __restrict__ best_idx,
+                                        double* __restrict__ scratch) {
+    const int64_t cnt = (int64_t)*done_cnt;
+    if (cnt > done_cap) return;
+    const int64_t gthread = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double* my_scratch = scratch + gthread * 2 * (int64_t)(2 * a.w + 1);
+    for (int64_t k = gthread; k < cnt; k += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long x = list[k];
+        rescore_entry<T, DMAX>(a, (int64_t)(x >> 40), (int64_t)(x & ((1ull << 40) - 1)), cand_of, res, minv, dbest_in,
+                               pass, min64, best_idx, my_scratch);
     }
 }
 
@@ -1672,7 +1766,9 @@ struct Plan {
     bool has_lb, exact;
     int64_t max_tiles;
     // byte offsets
-    size_t o_qT, o_ub;
+    size_t o_qT, o_ub, o_done;
+    int64_t done_cap, ub_sampled;
+    int ub_ct, ub_stride;
     size_t o_up, o_lo, o_upT, o_loT, o_candT, o_steps, o_blo, o_bhi, o_bcnt, o_lb, o_seed, o_seedres,
         o_seedcnt, o_dbest, o_ccnt, o_coff, o_surv, o_res, o_tcnt, o_toff, o_tq, o_tb, o_tl, o_sq, o_sb, o_sl,
         o_ctr, o_minv, o_min64, o_bidx, o_tctr, o_cub, o_fsc, o_tisc, total;
@@ -1757,6 +1853,20 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     p.o_min64 = take((size_t)Q * 8);
     p.o_bidx = take((size_t)Q * 8);
     p.o_tctr = take(16 * sizeof(int));
+    p.done_cap = Q * 256 + 65536;
+    // UB (seeding only) on every ub_stride-th candidate tile of the LB_MV pass
+    p.ub_ct = p.exact ? MvTile<double, 8, true>::CT : MvTile<float, 8, false>::CT;
+    {
+        const int64_t tiles = (N + p.ub_ct - 1) / p.ub_ct;
+        int64_t st = tiles / 256;
+        p.ub_stride = (int)(st < 1 ? 1 : (st > 8 ? 8 : st));
+        if (p.exact && p.d > 8) p.ub_ct = MvTile<double, 16, true>::CT;
+        const int64_t full = (N / ((int64_t)p.ub_ct * p.ub_stride)) * p.ub_ct;
+        const int64_t rem = N % ((int64_t)p.ub_ct * p.ub_stride);
+        p.ub_sampled = full + (rem < p.ub_ct ? rem : p.ub_ct);
+    }
+    if (const char* cap = getenv("TCDTW_DONE_CAP")) p.done_cap = atoll(cap);  // tests: force the overflow path
+    p.o_done = take((size_t)p.done_cap * 8 + 64);
     size_t b1 = 0, b2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b1, (int64_t*)nullptr, (int64_t*)nullptr, (int)(Q * p.n_chunks + 1));
     b2 = b1;
@@ -1866,6 +1976,9 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
         a.casc_thr = (T)1.0;  // thr already carries the (1+3 eps) margin
     }
     a.abandon = dsc->method != TCDTW_METHOD_NONE;
+    a.done_list = nullptr;  // set for the survivors pass only
+    a.done_cnt = nullptr;
+    a.done_cap = 0;
     return a;
 }
 
@@ -1949,20 +2062,20 @@ struct SearchImpl {
         if (p.has_lb)
             TRY((launch_lbmv_matrix<T, DMAX, EXACT>(at<T>(ws, p.o_upT), at<T>(ws, p.o_loT), at<T>(ws, p.o_qT),
                                                     at<T>(ws, p.o_candT), p.Q, p.N, p.n, p.d, at<T>(ws, p.o_lb),
-                                                    at<T>(ws, p.o_ub), st)));
+                                                    at<T>(ws, p.o_ub), st, p.ub_stride)));
         dbg_stage(st, "lb_mv");
         tm.mark(2);
         if (p.S > 0) {
             uint32_t* seeds = at<uint32_t>(ws, p.o_seed);
             int32_t* scnt = at<int32_t>(ws, p.o_seedcnt);
-            const int s_eff = (int)(p.S < p.N ? p.S : p.N);
+            const int s_eff = (int)(p.S < p.ub_sampled ? p.S : p.ub_sampled);
             switch (p.S) {
-                case 1: topk_kernel<T, 1><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
-                case 2: topk_kernel<T, 2><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
-                case 4: topk_kernel<T, 4><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
-                case 8: topk_kernel<T, 8><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
-                case 16: topk_kernel<T, 16><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
-                default: topk_kernel<T, 32><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt); break;
+                case 1: topk_kernel<T, 1><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt, p.ub_ct, p.ub_stride); break;
+                case 2: topk_kernel<T, 2><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt, p.ub_ct, p.ub_stride); break;
+                case 4: topk_kernel<T, 4><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt, p.ub_ct, p.ub_stride); break;
+                case 8: topk_kernel<T, 8><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt, p.ub_ct, p.ub_stride); break;
+                case 16: topk_kernel<T, 16><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt, p.ub_ct, p.ub_stride); break;
+                default: topk_kernel<T, 32><<<(unsigned)p.Q, 256, 0, st>>>(at<T>(ws, p.o_ub), p.N, s_eff, a.dbest, seeds, scnt, p.ub_ct, p.ub_stride); break;
             }
             TRY(launch_status());
             Tiles stl{at<uint32_t>(ws, p.o_sq), at<int64_t>(ws, p.o_sb), at<int32_t>(ws, p.o_sl)};
@@ -2043,7 +2156,14 @@ struct SearchImpl {
         }
         dbg_stage(st, "advanced");
         tm.mark(6);
-        TRY((launch_dtw<T, DMAX, EXACT>(a, p, tl, n_tiles, surv, res, at<int>(ws, p.o_tctr), st)));
+        unsigned long long* done_cnt = at<unsigned long long>(ws, p.o_done);
+        unsigned long long* done_list = done_cnt + 8;
+        cudaMemsetAsync(done_cnt, 0, 8, st);
+        SArgs<T> ad = a;
+        ad.done_list = done_list;
+        ad.done_cnt = done_cnt;
+        ad.done_cap = p.done_cap;
+        TRY((launch_dtw<T, DMAX, EXACT>(ad, p, tl, n_tiles, surv, res, at<int>(ws, p.o_tctr), st)));
         dbg_stage(st, "dtw");
         tm.mark(7);
         // finalize
@@ -2059,11 +2179,15 @@ struct SearchImpl {
         const T* seedres = at<T>(ws, p.o_seedres);
         const int fgrid = sms * 4;
         if (p.S > 0) {
-            fin_min_kernel<T><<<fgrid, 256, 0, st>>>(stl, p.Q, seedres, minv);
+            fin_min_kernel<T><<<fgrid, 256, 0, st>>>(stl, p.Q, seedres, minv, nullptr, 0);
             TRY(launch_status());
         }
         if (n_tiles > 0) {
-            fin_min_kernel<T><<<fgrid, 256, 0, st>>>(tl, n_tiles, res, minv);
+            // completed survivors from the list; the full tile scan only if
+            // the list overflowed (both decided on the device)
+            fin_min_list_kernel<T><<<fgrid, 256, 0, st>>>(done_list, done_cnt, p.done_cap, res, minv);
+            TRY(launch_status());
+            fin_min_kernel<T><<<fgrid, 256, 0, st>>>(tl, n_tiles, res, minv, done_cnt, p.done_cap);
             TRY(launch_status());
         }
         const T* dbi = (const T*)dbest_in;
@@ -2072,12 +2196,15 @@ struct SearchImpl {
         for (int pass = EXACT ? 1 : 0; pass < 2; ++pass) {
             if (p.S > 0) {
                 fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, stl, p.Q, seeds, seedres, minv, dbi, pass,
-                                                                   min64, bidx, fsc);
+                                                                   min64, bidx, fsc, nullptr, 0);
                 TRY(launch_status());
             }
             if (n_tiles > 0) {
+                fin_rescore_list_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, done_list, done_cnt, p.done_cap, surv, res,
+                                                                        minv, dbi, pass, min64, bidx, fsc);
+                TRY(launch_status());
                 fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, tl, n_tiles, surv, res, minv, dbi, pass, min64,
-                                                                   bidx, fsc);
+                                                                   bidx, fsc, done_cnt, p.done_cap);
                 TRY(launch_status());
             }
         }

@@ -275,3 +275,12 @@ def test_sharded_combine_equals_single(P):
         assert np.array_equal(idx, ref.best_index)
         assert np.array_equal(best, ref.best_distance)
     del torch
+
+
+def test_completed_list_overflow_path(P, monkeypatch):
+    """Finalisation normally visits only the list of completed DTWs; with a
+    capacity of 1 it must fall back to scanning every survivor tile and still
+    return the same answers."""
+    monkeypatch.setenv("TCDTW_DONE_CAP", "1")
+    _oracle_check(P, "C1", 0, 24, rel=0.0)
+    _oracle_check(P, "C0", 0, 20, rel=0.0)
