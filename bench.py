@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--window-index", type=int, default=0)
-    ap.add_argument("--method", default="tc_dtw")
+    ap.add_argument("--method", default="lb_mv")
     ap.add_argument("--queries", type=int, default=0, help="use only the first Q queries (0 = all)")
     ap.add_argument("--candidates", type=int, default=0, help="override N_c (0 = config)")
     ap.add_argument("--batch", type=int, default=0)
@@ -183,7 +183,7 @@ def run_reference(args):
     w = wl.spec.windows()[args.window_index]
     method, advanced = args.method, None
     if method == "tc_dtw":
-        advanced = os.environ.get("TCDTW_REF_ADVANCED", "lb_pc")
+        advanced = os.environ.get("TCDTW_REF_ADVANCED", "lb_pc")  # the GPU arm's tc_dtw_select pick on C4
     del core
     from oracle import oracle as O
 

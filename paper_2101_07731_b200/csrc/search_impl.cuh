@@ -562,6 +562,7 @@ struct SArgs {
     unsigned long long* done_list;
     unsigned long long* done_cnt;
     int64_t done_cap;
+    int refill_min;  // lane kernel: refill once at least this many lanes are free
 };
 
 template <typename T>
@@ -1007,6 +1008,9 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
     // refill free lanes; a new pair starts with `prev` as its row -1 band
     auto refill = [&](T (&prev)[B]) {
         unsigned freem = __ballot_sync(FULL, !busy);
+        // the refill path costs the whole warp its instructions however many
+        // lanes it serves: batch it until refill_min lanes are free
+        if (__popc(freem) < a.refill_min && freem != FULL) return;
         while (freem && !exhausted) {
             if (t_next >= t_len) {
                 int64_t tile = 0;
@@ -1976,6 +1980,8 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
         a.casc_thr = (T)1.0;  // thr already carries the (1+3 eps) margin
     }
     a.abandon = dsc->method != TCDTW_METHOD_NONE;
+    a.refill_min = 8;
+    if (const char* rm = getenv("TCDTW_REFILL_MIN")) a.refill_min = atoi(rm);
     a.done_list = nullptr;  // set for the survivors pass only
     a.done_cnt = nullptr;
     a.done_cap = 0;
