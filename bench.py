@@ -115,6 +115,20 @@ class ClockSampler:
         return out
 
 
+def traffic_from_profile(cells_per_launch=None):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the
+    committed ncu --set full capture (profiles/dtw_lane_traffic.json, taken
+    on a reduced C4 run) scaled by DP cells per launch; None if absent."""
+    p = ROOT / "profiles" / "dtw_lane_traffic.json"
+    if p.exists() and cells_per_launch:
+        try:
+            j = json.loads(p.read_text())
+            return j["dram_bytes"] / j["dtw_cells"] * cells_per_launch
+        except Exception:
+            pass
+    return None
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -345,8 +359,9 @@ def run_ours(args):
     else:
         ops = dtw_cells * (2 * d + 4)
         achieved = ops / (dtw_ms / 1e3) / 1e12
-        roof = {"kernel": "dtw_tpp_kernel", "bound": "alu", "achieved": achieved, "peak": alu_peak,
-                "unit": "Tlane-op/s", "frac": achieved / alu_peak, "traffic": None}
+        roof = {"kernel": "dtw_lane_kernel", "bound": "alu", "achieved": achieved, "peak": alu_peak,
+                "unit": "Tlane-op/s", "frac": achieved / alu_peak, "traffic": traffic_from_profile(dtw_cells / max(1, -(-n_q // batch))),
+                "algorithmic_ops": f"(2d+4) = {2 * d + 4} per DP cell x {dtw_cells:.4g} cells (SURVEY 8d)"}
     roof["peak_source"] = ("tcdtw_alu_probe FFMA issue rate measured in this run (nominal 148 SM x 128 lanes x "
                            f"{measured_peaks().get('sm_max_mhz', 1965)} MHz = "
                            f"{148 * 128 * measured_peaks().get('sm_max_mhz', 1965) / 1e6:.1f} T)")

@@ -137,14 +137,16 @@ struct MvTile {
     static constexpr int CT = 16 * M;
 };
 
-template <typename T, int DMAX, bool EXACT, bool UB>
+template <typename T, int DMAX, bool EXACT, bool UB, int DX>
 __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT, const T* __restrict__ LT,
                                                         const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                         int64_t Q, int64_t N, int n, int d, int TC,
                                                         T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
                                                         int64_t c0);
 
-template <typename T, int DMAX, bool EXACT, bool UB>
+// DX > 0: the dimension count is a compile-time constant (fully unrolled
+// per-dimension loop for the hot shapes); DX == 0: runtime d.
+template <typename T, int DMAX, bool EXACT, bool UB, int DX>
 __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ UT, const T* __restrict__ LT,
                                                           const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                           int64_t Q, int64_t N, int n, int d, int TC,
@@ -161,14 +163,14 @@ __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ 
     // candidate tile (block-uniform)
     if constexpr (UB) {
         if (((int64_t)blockIdx.x / nqt) % ub_stride != 0) {
-            lbmv_matrix_kernel_body<T, DMAX, EXACT, false>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0);
+            lbmv_matrix_kernel_body<T, DMAX, EXACT, false, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0);
             return;
         }
     }
-    lbmv_matrix_kernel_body<T, DMAX, EXACT, UB>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0);
+    lbmv_matrix_kernel_body<T, DMAX, EXACT, UB, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0);
 }
 
-template <typename T, int DMAX, bool EXACT, bool UB>
+template <typename T, int DMAX, bool EXACT, bool UB, int DX>
 __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT, const T* __restrict__ LT,
                                                         const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                         int64_t Q, int64_t N, int n, int d, int TC,
@@ -254,8 +256,10 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
                 for (int i = 0; i < M; ++i)
 #pragma unroll
                     for (int j = 0; j < M; ++j) s[i][j] = sd[i][j] = T(0);
-                for (int p = 0; p < d; ++p) {
-                    const int r = tt * d + p;
+                constexpr int PU = DX > 0 ? DX : 1;
+#pragma unroll PU
+                for (int p = 0; p < (DX > 0 ? DX : d); ++p) {
+                    const int r = tt * (DX > 0 ? DX : d) + p;
                     T u[M], l[M], c[M], qv[M];
                     if constexpr (M == 4 && sizeof(T) == 4) {
                         const float4 u4 = *reinterpret_cast<const float4*>(us + r * QT + tq * 4);
@@ -326,7 +330,15 @@ int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int6
     TC = TC < 1 ? 1 : (TC > 16 ? 16 : TC);
     TC = TC > n ? n : TC;
     const size_t smem = per_t * TC;
-    auto kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true> : lbmv_matrix_kernel<T, DMAX, EXACT, false>;
+    auto kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true, 0> : lbmv_matrix_kernel<T, DMAX, EXACT, false, 0>;
+    if constexpr (!EXACT) {
+#define TCDTW_MV_DX(DD)                                                                                    \
+        if (d == DD && DD <= DMAX)                                                                         \
+            kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true, (DD <= DMAX ? DD : 0)>                      \
+                      : lbmv_matrix_kernel<T, DMAX, EXACT, false, (DD <= DMAX ? DD : 0)>;
+        TCDTW_MV_DX(3) TCDTW_MV_DX(4) TCDTW_MV_DX(5) TCDTW_MV_DX(6) TCDTW_MV_DX(8) TCDTW_MV_DX(20)
+#undef TCDTW_MV_DX
+    }
     if (smem > 48 * 1024) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return TCDTW_CUDA_ERROR;
