@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exchange", action="store_true", help="skip the d_best all-reduce between phases")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (testing)")
     return ap.parse_args()
 
 
@@ -240,8 +241,12 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dev = local if args.dist_backend == "nccl" else local % torch.cuda.device_count()
+        torch.cuda.set_device(dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(args.dist_backend)
     else:
         torch.cuda.set_device(0)
     import paper_2101_07731_b200 as P
@@ -302,7 +307,7 @@ def run_ours(args):
         step(Qdev)
     torch.cuda.synchronize()
     launches0 = L.tcdtw_launch_count() if hasattr(L, "tcdtw_launch_count") else 0
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         times = timed(lambda: step(Qdev), args.steps)
     launches = (L.tcdtw_launch_count() - launches0) if hasattr(L, "tcdtw_launch_count") else None
     clocks = clk.summary()
