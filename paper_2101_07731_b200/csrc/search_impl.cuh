@@ -899,6 +899,9 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
     constexpr int W = (B - 1) / 2;
     constexpr int DP = (D + 1) / 2;     // coordinate pairs per point
     constexpr bool QV = (D % 2 == 0);   // query/envelope rows as pairs
+    // large d: do not carry the next step's query columns and envelope rows
+    // across steps (register budget); load them inside the step instead
+    constexpr bool LEAN = D > 8;
     using T2 = typename Vec8<T>::type;
     using PL = PairLoad<T, D>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1092,11 +1095,13 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
                 for (int k = W; k < B; ++k)
 #pragma unroll
                     for (int pp = 0; pp < DP; ++pp) ring[(k * DP + pp) * 32] = qstage[(k - W) * DP + pp];
-                load_col(x1, W + 1);
-                load_col(x2, W + 2);
-                if (casc) {
-                    load_env(eu0, el0, 0);
-                    load_env(eu1, el1, 1 < n ? 1 : 0);
+                if constexpr (!LEAN) {
+                    load_col(x1, W + 1);
+                    load_col(x2, W + 2);
+                    if (casc) {
+                        load_env(eu0, el0, 0);
+                        load_env(eu1, el1, 1 < n ? 1 : 0);
+                    }
                 }
 #pragma unroll
                 for (int p = 0; p < D; ++p) {
@@ -1123,9 +1128,17 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
     auto step = [&](T (&P)[B], T (&N)[B]) {
         const bool two = (i + 1 < n);
         T rmin0, rmin1;
+        if constexpr (LEAN) load_col(x1, i + W + 1);
         dtw_step2<T, D, B, EXACT>(P, N, c0, c1, ring, h, x1, rmin0, rmin1);
+        if constexpr (LEAN) load_col(x2, i + W + 2);
         // cascade terms of rows i, i+1 from envelope rows loaded a step ago
         T suf0 = T(0), suf1 = T(0);
+        if constexpr (LEAN) {
+            if (casc) {
+                load_env(eu0, el0, i);
+                load_env(eu1, el1, i + 1 < n ? i + 1 : i);
+            }
+        }
         if (casc) {
             prefix += lb_term(c0, eu0, el0);
             suf0 = tmax(lbtot * a.casc_lo - prefix * a.casc_hi, T(0));
@@ -1190,11 +1203,13 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
             }
         }
         // operands of the next step, consumed after its DP
-        load_col(x1, i + W + 1);
-        load_col(x2, i + W + 2);
-        if (casc) {
-            load_env(eu0, el0, i);
-            load_env(eu1, el1, i + 1 < n ? i + 1 : i);
+        if constexpr (!LEAN) {
+            load_col(x1, i + W + 1);
+            load_col(x2, i + W + 2);
+            if (casc) {
+                load_env(eu0, el0, i);
+                load_env(eu1, el1, i + 1 < n ? i + 1 : i);
+            }
         }
         since += 2;
         if (since >= 8) {
@@ -1224,7 +1239,7 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
 // C4: (float,6,25).
 #define TCDTW_LANE_SPECS(X) \
     X(float, 3, 25) X(float, 4, 25) X(float, 5, 25) X(float, 6, 25) X(float, 8, 25) \
-    X(float, 3, 13) X(float, 5, 13) X(float, 6, 13) X(float, 8, 13) X(double, 3, 25)
+    X(float, 3, 13) X(float, 5, 13) X(float, 6, 13) X(float, 8, 13) X(float, 20, 13) X(double, 3, 25)
 
 template <typename T>
 static int launch_lane(const SArgs<T>& a, int d, int B, Tiles tl, int64_t n_tiles, const uint32_t* cand_of, T* res,
@@ -1725,6 +1740,167 @@ __global__ void fin_rescore_list_kernel(SArgs<T> a, const unsigned long long* __
     }
 }
 
+// --- finalists: collected once, re-scored by one warp each, picked ----------
+// A finalist is a completed DTW whose float32 value is within the margin of
+// the best (FAST), or equal to the best (EXACT).  (q << 40 | entry) with the
+// candidate index kept alongside.
+struct Finalists {
+    unsigned long long* item;  // (q << 40) | candidate
+    double* d64;               // float64 DTW (FAST) / stored value (EXACT)
+    unsigned long long* cnt;
+    int64_t cap;
+};
+
+template <typename T>
+__device__ __forceinline__ void collect_entry(const SArgs<T>& a, int64_t q, T r, uint32_t c,
+                                              const T* __restrict__ minv, const T* __restrict__ dbest_in,
+                                              Finalists f) {
+    if (!(r >= T(0)) || r == dev_inf<T>()) return;
+    bool take;
+    if constexpr (sizeof(T) == 8) {
+        take = (r == minv[q]);
+    } else {
+        T bound = minv[q];
+        if (dbest_in) bound = tmin(bound, dbest_in[q]);
+        take = r <= __fmul_ru(bound, a.mg.fin);
+    }
+    if (!take) return;
+    const unsigned long long k = atomicAdd(f.cnt, 1ull);
+    if ((int64_t)k < f.cap) {
+        f.item[k] = ((unsigned long long)q << 40) | (unsigned long long)c;
+        f.d64[k] = (double)r;
+    }
+}
+
+// seeds (tile list) and the completed survivors (done list) -> finalists
+template <typename T>
+__global__ void fin_collect_kernel(SArgs<T> a, Tiles stl, int64_t n_seed_tiles, const uint32_t* __restrict__ seeds,
+                                   const T* __restrict__ seedres, const unsigned long long* __restrict__ list,
+                                   const unsigned long long* __restrict__ done_cnt, int64_t done_cap,
+                                   const uint32_t* __restrict__ cand_of, const T* __restrict__ res,
+                                   const T* __restrict__ minv, const T* __restrict__ dbest_in, Finalists f) {
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = gt; k < n_seed_tiles * 32; k += stride) {
+        const int64_t tile = k >> 5;
+        const int lane = (int)(k & 31);
+        if (lane < stl.len[tile]) {
+            const int64_t ent = stl.begin[tile] + lane;
+            collect_entry<T>(a, stl.q[tile], seedres[ent], seeds[ent], minv, dbest_in, f);
+        }
+    }
+    if (list == nullptr) return;
+    const int64_t cnt = (int64_t)*done_cnt;
+    if (cnt > done_cap) return;
+    for (int64_t k = gt; k < cnt; k += stride) {
+        const unsigned long long x = list[k];
+        const int64_t q = (int64_t)(x >> 40), ent = (int64_t)(x & ((1ull << 40) - 1));
+        collect_entry<T>(a, q, res[ent], cand_of[ent], minv, dbest_in, f);
+    }
+}
+
+// EXACT float64 DTW of one (query, candidate) pair by one warp: lane = row of
+// a 32-row chunk, anti-diagonal skew of 2 per lane, one shuffle per step, the
+// chunk's last row handed over through shared memory (prow, 2W+1 doubles).
+// Same per-cell arithmetic as dtw_banded (numpy order, no contraction).
+template <typename TIn, int DMAX>
+__device__ double dtw_warp_exact(const TIn* __restrict__ rows_s, const TIn* __restrict__ cols_s, int n, int d,
+                                 int w, double* prow) {
+    const int lane = threadIdx.x & 31;
+    const int B = 2 * w + 1;
+    const double INF = dev_inf<double>();
+    for (int k = lane; k < B; k += 32) prow[k] = (k == w) ? 0.0 : INF;
+    __syncwarp();
+    double fin = INF;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        const bool valid = i < n;
+        double rp[DMAX];
+#pragma unroll
+        for (int p = 0; p < DMAX; ++p) rp[p] = (valid && p < d) ? (double)rows_s[(int64_t)i * d + p] : 0.0;
+        double mine = INF, got = INF;
+        const int steps = B + 62;
+        for (int tau = 0; tau < steps; ++tau) {
+            const int k = tau - 2 * lane;
+            const double got_prev = got;
+            got = __shfl_up_sync(0xffffffffu, mine, 1);
+            const bool act = valid && k >= 0 && k < B;
+            double v = INF;
+            if (act) {
+                double up, dg;
+                if (lane == 0) {
+                    up = (k + 1 < B) ? prow[k + 1] : INF;
+                    dg = prow[k];
+                } else {
+                    up = got;
+                    dg = got_prev;
+                }
+                const int j = i - w + k;
+                double cost = INF;
+                if (j >= 0 && j < n) {
+                    double sq[DMAX];
+#pragma unroll
+                    for (int p = 0; p < DMAX; ++p) {
+                        if (p < d) {
+                            const double df = __dsub_rn(rp[p], (double)cols_s[(int64_t)j * d + p]);
+                            sq[p] = __dmul_rn(df, df);
+                        } else {
+                            sq[p] = 0.0;
+                        }
+                    }
+                    cost = __dsqrt_rn(np_sum<double, DMAX>(sq, d));
+                }
+                const double best = fmin(fmin(up, dg), mine);
+                v = __dadd_rn(cost, best);
+                if (i == n - 1 && k == w) fin = v;
+            }
+            mine = v;
+            __syncwarp();
+            if (act && lane == 31) prow[k] = v;
+            __syncwarp();
+        }
+    }
+    return __shfl_sync(0xffffffffu, fin, (n - 1) & 31);
+}
+
+template <typename T, int DMAX>
+__global__ void fin_rescore_warp_kernel(SArgs<T> a, Finalists f, unsigned long long* __restrict__ min64) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* prow = reinterpret_cast<double*>(smem_raw) + (size_t)wib * (2 * a.w + 1);
+    const int64_t cnt = min((int64_t)*f.cnt, f.cap);
+    for (int64_t k = blockIdx.x * (int64_t)warps + wib; k < cnt; k += (int64_t)gridDim.x * warps) {
+        const unsigned long long x = f.item[k];
+        const int64_t q = (int64_t)(x >> 40), c = (int64_t)(x & ((1ull << 40) - 1));
+        double d64;
+        if constexpr (sizeof(T) == 8) {
+            d64 = f.d64[k];  // EXACT: the stored value is the reference's
+        } else {
+            // DTW is symmetric (test_dtw.py:196-207): rows = candidate
+            d64 = dtw_warp_exact<T, DMAX>(a.cands + c * (int64_t)a.n * a.d, a.queries + q * (int64_t)a.n * a.d,
+                                          a.n, a.d, a.w, prow);
+        }
+        if (lane == 0) {
+            f.d64[k] = d64;
+            atomicMin(min64 + q, (unsigned long long)__double_as_longlong(d64));
+            if constexpr (sizeof(T) == 4)
+                atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + q * TCDTW_COUNTERS + TCDTW_C_FINALISTS),
+                          1ull);
+        }
+    }
+}
+
+static __global__ void fin_pick_kernel(Finalists f, const unsigned long long* __restrict__ min64,
+                                unsigned long long* __restrict__ best_idx) {
+    const int64_t cnt = min((int64_t)*f.cnt, f.cap);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < cnt; k += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long x = f.item[k];
+        const int64_t q = (int64_t)(x >> 40);
+        if ((unsigned long long)__double_as_longlong(f.d64[k]) == min64[q])
+            atomicMin(best_idx + q, x & ((1ull << 40) - 1));
+    }
+}
+
 template <typename T>
 __global__ void fin_output_kernel(int64_t Q, int64_t N, int64_t base, const T* __restrict__ minv,
                                   const unsigned long long* __restrict__ min64,
@@ -1782,8 +1958,8 @@ struct Plan {
     bool has_lb, exact;
     int64_t max_tiles;
     // byte offsets
-    size_t o_qT, o_ub, o_done;
-    int64_t done_cap, ub_sampled;
+    size_t o_qT, o_ub, o_done, o_fin;
+    int64_t done_cap, ub_sampled, fin_cap;
     int ub_ct, ub_stride;
     size_t o_up, o_lo, o_upT, o_loT, o_candT, o_steps, o_blo, o_bhi, o_bcnt, o_lb, o_seed, o_seedres,
         o_seedcnt, o_dbest, o_ccnt, o_coff, o_surv, o_res, o_tcnt, o_toff, o_tq, o_tb, o_tl, o_sq, o_sb, o_sl,
@@ -1883,6 +2059,8 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     }
     if (const char* cap = getenv("TCDTW_DONE_CAP")) p.done_cap = atoll(cap);  // tests: force the overflow path
     p.o_done = take((size_t)p.done_cap * 8 + 64);
+    p.fin_cap = p.done_cap + Q * kSeedMax;
+    p.o_fin = take((size_t)p.fin_cap * 16 + 64);
     size_t b1 = 0, b2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b1, (int64_t*)nullptr, (int64_t*)nullptr, (int)(Q * p.n_chunks + 1));
     b2 = b1;
@@ -2211,20 +2389,31 @@ struct SearchImpl {
         const T* dbi = (const T*)dbest_in;
         double* fsc = at<double>(ws, p.o_fsc);
         const int rgrid = p.fin_threads / 256;
-        for (int pass = EXACT ? 1 : 0; pass < 2; ++pass) {
-            if (p.S > 0) {
-                fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, stl, p.Q, seeds, seedres, minv, dbi, pass,
-                                                                   min64, bidx, fsc, nullptr, 0);
-                TRY(launch_status());
-            }
-            if (n_tiles > 0) {
-                fin_rescore_list_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, done_list, done_cnt, p.done_cap, surv, res,
-                                                                        minv, dbi, pass, min64, bidx, fsc);
-                TRY(launch_status());
-                fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, tl, n_tiles, surv, res, minv, dbi, pass, min64,
-                                                                   bidx, fsc, done_cnt, p.done_cap);
-                TRY(launch_status());
-            }
+        // finalists: seeds + completed survivors -> one warp per float64 re-score
+        Finalists F;
+        F.cnt = at<unsigned long long>(ws, p.o_fin);
+        F.item = F.cnt + 8;
+        F.d64 = reinterpret_cast<double*>(F.item + p.fin_cap);
+        F.cap = p.fin_cap;
+        cudaMemsetAsync(F.cnt, 0, 8, st);
+        fin_collect_kernel<T><<<fgrid, 256, 0, st>>>(a, stl, p.S > 0 ? p.Q : 0, seeds, seedres,
+                                                     n_tiles > 0 ? done_list : nullptr, done_cnt, p.done_cap, surv,
+                                                     res, minv, dbi, F);
+        TRY(launch_status());
+        fin_rescore_warp_kernel<T, DMAX><<<sms * 4, 256, (size_t)8 * (2 * p.w + 1) * sizeof(double), st>>>(a, F, min64);
+        TRY(launch_status());
+        // survivors' completed list overflowed: scan every tile instead
+        if (n_tiles > 0) {
+            fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, tl, n_tiles, surv, res, minv, dbi, EXACT ? 1 : 0,
+                                                               min64, bidx, fsc, done_cnt, p.done_cap);
+            TRY(launch_status());
+        }
+        fin_pick_kernel<<<fgrid, 256, 0, st>>>(F, min64, bidx);
+        TRY(launch_status());
+        if (n_tiles > 0 && !EXACT) {
+            fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, tl, n_tiles, surv, res, minv, dbi, 1, min64, bidx,
+                                                               fsc, done_cnt, p.done_cap);
+            TRY(launch_status());
         }
         fin_output_kernel<T><<<grid_for(p.Q, 256), 256, 0, st>>>(p.Q, p.N, dsc->candidate_base, minv, min64, bidx,
                                                                 a.counters, p.has_lb ? 1 : 0, best_index,
