@@ -1402,6 +1402,151 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
     }
 }
 
+// ------------------- DTW, warp per pair, continuous row pipeline (W >= 32)
+// Lane l owns rows l, l+32, l+64, ...; row r = l + 32m sweeps its 2W+1 band
+// columns in consecutive steps starting at S(r) = m(2W+1) + 2l, so lanes stay
+// busy back to back (no drain between 32-row chunks when 2W+1 >= 64).  The
+// cell above comes from lane l-1 one step earlier (one shuffle), the diagonal
+// from two steps earlier; lane 0 reads row r-1 (lane 31's previous row) from
+// a per-warp handoff row in shared memory.  Query rows are staged once per
+// block tile with an odd word stride (conflict-free column reads).  Rows
+// finish strictly in order, one per step at most, so the first row whose
+// minimum exceeds the threshold is found exactly (row-granular abandoning).
+template <typename T>
+__host__ __device__ inline int pipe_stride(int d) {  // odd number of 4-byte words per query row
+    if (sizeof(T) == 4) return (d % 2 == 1) ? d : d + 1;
+    return (d % 2 == 1) ? d : d + 1;  // doubles: odd count of 8-byte words
+}
+
+template <typename T, int DMAX, bool EXACT>
+__global__ void __launch_bounds__(256) dtw_pipe_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
+                                                       const uint32_t* __restrict__ cand_of, T* __restrict__ res,
+                                                       int* __restrict__ tile_ctr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int n = a.n, d = a.d, w = a.w, B = 2 * w + 1;
+    const int SP = pipe_stride<T>(d);
+    const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* qs = reinterpret_cast<T*>(smem_raw);                  // n * SP
+    T* hb = qs + (size_t)n * SP + (size_t)wib * (n + 1);     // per warp: row r-1 for lane 0 (index j+1)
+    __shared__ int64_t tile_s;
+    const T INF = dev_inf<T>();
+    const unsigned FULL = 0xffffffffu;
+    const int src = (lane + 31) & 31;
+    int64_t cached_q = -1;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1);
+        __syncthreads();
+        const int64_t tile = tile_s;
+        if (tile >= n_tiles) break;
+        const int64_t q = tl.q[tile];
+        const int64_t e0 = tl.begin[tile];
+        const int len = tl.len[tile];
+        if (q != cached_q) {
+            const T* qsrc = a.queries + q * (int64_t)n * d;
+            for (int e = threadIdx.x; e < n * d; e += blockDim.x) {
+                const int r = e / d, p = e - (e / d) * d;
+                qs[r * SP + p] = qsrc[e];
+            }
+            cached_q = q;
+            __syncthreads();
+        }
+        for (int slot = wib; slot < len; slot += warps) {
+            const int64_t ent = e0 + slot;
+            if (res[ent] < T(0)) continue;  // pruned by the advanced bound (warp-uniform)
+            const int64_t c = cand_of[ent];
+            const T* crow = a.cands + c * (int64_t)n * d;
+            T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg.prune) : INF;
+            int r = lane;                 // this lane's current row
+            int k = -2 * lane;            // slot within the row (negative: not started)
+            T rp[DMAX], rnext[DMAX];
+            load_point<T, DMAX>(rp, crow + (int64_t)(r < n ? r : 0) * d, d);
+            load_point<T, DMAX>(rnext, crow + (int64_t)(r + 32 < n ? r + 32 : 0) * d, d);
+            T mine = INF, got = INF, rmin = INF, fin = INF;
+            bool abandoned = false;
+            int stop_row = n - 1;
+            const int last_step = ((n - 1) / 32) * B + 2 * ((n - 1) & 31) + B;  // step after row n-1 ends
+            for (int tau = 0; tau < last_step; ++tau) {
+                const T got_prev = got;
+                got = __shfl_sync(FULL, mine, src);
+                const bool act = r < n && k >= 0;
+                T v = INF;
+                if (act) {
+                    const int j = r - w + k;
+                    T up, dg;
+                    if (lane == 0) {
+                        up = (r > 0 && k < B - 1 && j >= 0 && j < n) ? hb[j + 1] : INF;
+                        dg = (r > 0 && j >= 1 && j <= n) ? hb[j] : INF;
+                    } else {
+                        up = (k < B - 1) ? got : INF;
+                        dg = got_prev;
+                    }
+                    T best = tmin(tmin(up, dg), (k > 0) ? mine : INF);
+                    if (r == 0 && j == 0) best = T(0);
+                    T cost = INF;
+                    if (j >= 0 && j < n) {
+                        const T* qp = qs + j * SP;
+                        if constexpr (EXACT) {
+                            cost = dist_exact<T, DMAX>(rp, qp, d);
+                        } else {
+                            T s2 = T(0);
+#pragma unroll
+                            for (int p = 0; p < DMAX; ++p)
+                                if (p < d) {
+                                    const T df = rp[p] - qp[p];
+                                    s2 = fma(df, df, s2);
+                                }
+                            cost = fast_sqrt(s2);
+                        }
+                    }
+                    v = EXACT ? add_rn(cost, best) : cost + best;
+                    rmin = tmin(rmin, v);
+                    if (r == n - 1 && k == w) fin = v;
+                }
+                __syncwarp();
+                if (act && lane == 31 && r - w + k >= 0 && r - w + k < n) hb[r - w + k + 1] = v;  // to lane 0's next row
+                __syncwarp();
+                mine = v;
+                // row end: abandon test (rows end in order, at most one per step)
+                const bool row_end = act && k == B - 1;
+                const bool bad = row_end && rmin > thr;
+                const unsigned badm = __ballot_sync(FULL, bad);
+                if (badm) {
+                    abandoned = true;
+                    stop_row = __shfl_sync(FULL, r, __ffs(badm) - 1);
+                    break;
+                }
+                if (act) ++k;
+                else if (k < 0) ++k;
+                if (k == B) {  // next row of this lane
+                    k = 0;
+                    r += 32;
+                    rmin = INF;  // (mine keeps the last cell: lane l+1 still needs it next step)
+#pragma unroll
+                    for (int p = 0; p < DMAX; ++p) rp[p] = rnext[p];
+                    if (r + 32 < n) load_point<T, DMAX>(rnext, crow + (int64_t)(r + 32) * d, d);
+                }
+                if ((tau & 63) == 63 && a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg.prune);
+            }
+            fin = __shfl_sync(FULL, fin, (n - 1) & 31);
+            if (!abandoned && fin > thr) abandoned = true;  // dtw.py:101-102
+            if (lane == 0) {
+                res[ent] = abandoned ? INF : fin;
+                if (!abandoned) {
+                    atomic_min_nonneg<T>(a.dbest + q, fin);
+                    note_done(a, q, ent);
+                }
+                int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
+                atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_DTW_COMPUTED), 1ull);
+                if (abandoned) atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_ABANDON_COUNT), 1ull);
+                atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_DTW_CELLS),
+                          (unsigned long long)cells_upto(stop_row, n, w));
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // ------------------------------------------------- advanced bounds (step 2)
 // One lane per survivor, the tile's query shared by the warp; evaluated only
 // in the trigger band LB_MV > e * d_best (search.py:147).  A survivor whose
@@ -1581,6 +1726,129 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
         if (go && val > thr) res[ent] = T(-1);
         int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
         warp_add_counter(ctr + TCDTW_C_ADVANCED_LB_EVALS, go ? 1 : 0);
+    }
+}
+
+// ------------------------- LB_PC on survivors, boxes staged in shared memory
+// Warp per work tile (32 survivors of one query, lane = survivor).  The
+// query's box sets (G x K boxes, lb_pc.py:229-234 padding included) are staged
+// once per tile query in the warp's shared memory as (lo, hi) pairs; all lanes
+// walk the candidate index t in lockstep, so every box read is a broadcast.
+// Early exit once every lane's running sum exceeds the threshold.  FAST mode
+// only (the float64 path keeps advanced_kernel's exact arithmetic).
+template <typename T, int D, bool VEC>
+__global__ void __launch_bounds__(256) advanced_pc_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
+                                                          const uint32_t* __restrict__ cand_of, T* __restrict__ res,
+                                                          int* __restrict__ tile_ctr) {
+    using T2 = typename Vec8<T>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int n = a.n, G = a.G, K = a.K, gw = a.gw;
+    const int lane = threadIdx.x & 31;
+    T2* bx = reinterpret_cast<T2*>(smem_raw) + (size_t)(threadIdx.x >> 5) * G * K * D;  // [g][k][p] -> (lo, hi)
+    const T INF = dev_inf<T>();
+    const unsigned FULL = 0xffffffffu;
+    int64_t cached_q = -1;
+    while (true) {
+        int64_t tile = 0;
+        if (lane == 0) tile = atomicAdd(tile_ctr, 1);
+        tile = __shfl_sync(FULL, tile, 0);
+        if (tile >= n_tiles) break;
+        const int64_t q = tl.q[tile];
+        const int64_t ent = tl.begin[tile] + lane;
+        const bool has = lane < tl.len[tile];
+        if (q != cached_q) {
+            __syncwarp();
+            const T* bl = a.box_lo + q * (int64_t)G * K * D;
+            const T* bh = a.box_hi + q * (int64_t)G * K * D;
+            for (int e = lane; e < G * K * D; e += 32) bx[e] = T2{bl[e], bh[e]};
+            cached_q = q;
+            __syncwarp();
+        }
+        const int64_t c = has ? (int64_t)cand_of[ent] : 0;
+        const T db = load_volatile(a.dbest + q);
+        const T thr = scale_up<T>(db, a.mg.prune);
+        const T lb1 = has ? a.lb[q * a.N + c] : T(0);
+        const bool go = has && !(res[ent] < T(0)) && (lb1 > a.trigger * db);  // trigger band, search.py:147
+        const T* crow = a.cands + c * (int64_t)n * D;
+        using PL = PairLoad<T, D>;
+        T val = T(0);
+        // two candidate rows per pass: one vectorised load of 2D values
+        for (int t = 0; t < n && __any_sync(FULL, go && val <= thr); t += 2) {
+            T cp2[2 * D];
+            if (VEC && t + 1 < n) {
+                const typename PL::V* src = reinterpret_cast<const typename PL::V*>(crow + (int64_t)t * D);
+#pragma unroll
+                for (int v = 0; v < PL::nv; ++v) {
+                    const typename PL::V x = __ldg(src + v);
+                    const T* xs = reinterpret_cast<const T*>(&x);
+#pragma unroll
+                    for (int u = 0; u < PL::per; ++u) cp2[v * PL::per + u] = xs[u];
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 2 * D; ++u) cp2[u] = (t + u / D < n) ? __ldg(crow + (int64_t)t * D + u) : T(0);
+            }
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                if (t + r < n) {
+                    const T2* gb = bx + (size_t)((t + r) / gw) * K * D;
+                    T best = INF;
+                    for (int k = 0; k < K; ++k) {
+                        T acc = T(0);
+#pragma unroll
+                        for (int p = 0; p < D; ++p) {
+                            const T2 b = gb[k * D + p];
+                            const T cv = cp2[r * D + p];
+                            const T dv = tmax(tmax(b.x - cv, cv - b.y), T(0));
+                            acc = fma(dv, dv, acc);
+                        }
+                        best = tmin(best, acc);
+                    }
+                    val += fast_sqrt(best);
+                }
+            }
+        }
+        if (go && val > thr) res[ent] = T(-1);
+        int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
+        warp_add_counter(ctr + TCDTW_C_ADVANCED_LB_EVALS, go ? 1 : 0);
+    }
+}
+
+#define TCDTW_PC_DIMS(X) X(3) X(4) X(5) X(6) X(8) X(20)
+
+template <typename T>
+static int launch_advanced_pc(const SArgs<T>& a, int d, Tiles tl, int64_t n_tiles, const uint32_t* cand_of, T* res,
+                              int* tctr, cudaStream_t st) {
+    if constexpr (sizeof(T) == 8) {
+        return TCDTW_NOT_SUPPORTED;
+    } else {
+        auto go = [&](auto kern, int DD) -> int {
+            const size_t smem = (size_t)8 * a.G * a.K * DD * 2 * sizeof(T);
+            if (smem > 227 * 1024) return TCDTW_NOT_SUPPORTED;
+            if (smem > 48 * 1024 &&
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return TCDTW_NOT_SUPPORTED;
+            int dev = 0, sms = 148, occ = 1;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+            if (occ < 1) return TCDTW_NOT_SUPPORTED;
+            int64_t grid = (int64_t)occ * sms;
+            const int64_t need = (n_tiles + 7) / 8;
+            if (grid > need) grid = need;
+            cudaMemsetAsync(tctr, 0, sizeof(int), st);
+            kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
+            return launch_status();
+        };
+        const bool base_ok = (reinterpret_cast<uintptr_t>(a.cands) % 16) == 0;
+#define TCDTW_PC_CASE(DD)                                                                                   \
+        if (d == DD) {                                                                                      \
+            const bool vec = base_ok && (((int64_t)a.n * DD * sizeof(T)) % sizeof(typename PairLoad<T, DD>::V)) == 0; \
+            return vec ? go(advanced_pc_kernel<T, DD, true>, DD) : go(advanced_pc_kernel<T, DD, false>, DD); \
+        }
+        TCDTW_PC_DIMS(TCDTW_PC_CASE)
+#undef TCDTW_PC_CASE
+        return TCDTW_NOT_SUPPORTED;
     }
 }
 
@@ -2184,7 +2452,7 @@ template <typename T, int DMAX, bool EXACT>
 static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tiles, const uint32_t* cand_of, T* res,
                       int* tctr, cudaStream_t st) {
     if (n_tiles <= 0) return TCDTW_OK;
-    static const bool no_lane = getenv("TCDTW_NO_LANE") != nullptr;  // A/B switch for benchmarking
+    const bool no_lane = getenv("TCDTW_NO_LANE") != nullptr;  // A/B switch for benchmarking
     if (!no_lane) {
         const int s = launch_lane<T>(a, p.d, p.B, tl, n_tiles, cand_of, res, tctr, st);
         if (s != TCDTW_NOT_SUPPORTED) return s;
@@ -2212,6 +2480,23 @@ static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tile
         if (p.B <= 16) return run(dtw_tpp_kernel<T, DMAX, 16, EXACT>);
         if (p.B <= 32) return run(dtw_tpp_kernel<T, DMAX, 32, EXACT>);
         return run(dtw_tpp_kernel<T, DMAX, 64, EXACT>);
+    }
+    // continuous row pipeline: correct (tests/test_gpu_parity.py::test_long_band_shapes)
+    // but measured slower than the chunked wavefront on C1b/C3; opt-in
+    const bool use_pipe = getenv("TCDTW_PIPE") != nullptr;
+    if (p.w >= 32 && use_pipe) {
+        const size_t smem = ((size_t)p.n * pipe_stride<T>(p.d) + (size_t)8 * (p.n + 1)) * sizeof(T);
+        auto kern = dtw_pipe_kernel<T, DMAX, EXACT>;
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return TCDTW_NOT_SUPPORTED;
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+        if (occ < 1) return TCDTW_NOT_SUPPORTED;
+        int64_t grid = (int64_t)occ * sms;
+        if (grid > n_tiles) grid = n_tiles;
+        kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
+        return launch_status();
     }
     const size_t smem = ((size_t)(p.n + 2 * p.w) * p.d + (size_t)8 * p.B) * sizeof(T);
     auto kern = dtw_wave_kernel<T, DMAX, EXACT>;
@@ -2344,11 +2629,17 @@ struct SearchImpl {
         cudaStreamSynchronize(st);
         tm.mark(5);
         if (a.adv >= 0 && n_tiles > 0) {
-            cudaMemsetAsync(at<int>(ws, p.o_tctr), 0, sizeof(int), st);
-            int grid = (p.adv_warps * 32) / 256;
-            advanced_kernel<T, DMAX, EXACT><<<grid, 256, 0, st>>>(a, tl, n_tiles, surv, res, at<T>(ws, p.o_tisc),
-                                                                 at<int>(ws, p.o_tctr));
-            TRY(launch_status());
+            int sa = TCDTW_NOT_SUPPORTED;
+            if (a.adv == TCDTW_METHOD_LB_PC && !getenv("TCDTW_NO_PC_SMEM"))
+                sa = launch_advanced_pc<T>(a, p.d, tl, n_tiles, surv, res, at<int>(ws, p.o_tctr), st);
+            if (sa == TCDTW_NOT_SUPPORTED) {
+                cudaMemsetAsync(at<int>(ws, p.o_tctr), 0, sizeof(int), st);
+                int grid = (p.adv_warps * 32) / 256;
+                advanced_kernel<T, DMAX, EXACT><<<grid, 256, 0, st>>>(a, tl, n_tiles, surv, res, at<T>(ws, p.o_tisc),
+                                                                     at<int>(ws, p.o_tctr));
+                sa = launch_status();
+            }
+            TRY(sa);
         }
         dbg_stage(st, "advanced");
         tm.mark(6);

@@ -284,3 +284,25 @@ def test_completed_list_overflow_path(P, monkeypatch):
     monkeypatch.setenv("TCDTW_DONE_CAP", "1")
     _oracle_check(P, "C1", 0, 24, rel=0.0)
     _oracle_check(P, "C0", 0, 20, rel=0.0)
+
+
+@pytest.mark.parametrize("dt,n,d,w", [("f32", 256, 5, 51), ("f64", 256, 5, 51), ("f64", 256, 8, 51),
+                                      ("f32", 1024, 8, 102), ("f64", 512, 8, 102), ("f64", 1024, 8, 40),
+                                      ("f32", 200, 3, 70), ("f64", 97, 2, 33)])
+@pytest.mark.parametrize("pipe", [False, True])
+def test_long_band_shapes(P, dt, n, d, w, pipe, monkeypatch):
+    """Long bands (2W+1 > 64): wavefront kernels (and the opt-in row pipeline); ragged n (not
+    a multiple of 32) and rows near the end of the band are the edge cases."""
+    from oracle import oracle as O
+
+    if pipe:
+        monkeypatch.setenv("TCDTW_PIPE", "1")
+    rng = np.random.default_rng(n * 100 + w)
+    C = np.cumsum(rng.normal(size=(40, n, d)), axis=1)
+    Qs = np.cumsum(rng.normal(size=(3, n, d)), axis=1)
+    if dt == "f32":
+        C, Qs = C.astype(np.float32), Qs.astype(np.float32)
+    res = P.SearchIndex(C, dtype=dt).search(Qs, P.SearchParams(window=w, method="lb_mv"))
+    outs, _ = O.nn_search_batch(Qs.astype(np.float64), C.astype(np.float64), O.make_params(w, "lb_mv"), None, None)
+    assert res.best_index.tolist() == [o.best_index for o in outs]
+    assert res.best_distance.tolist() == [o.best_distance for o in outs]
