@@ -268,6 +268,10 @@ def run_ours(args):
     Qdev = index.prepare_queries(wl.queries)
     n_q = Qdev.shape[0]
     batch = args.batch or index.auto_batch(params, advanced, n_q, seeds=args.seeds)
+    if world > 1:  # every rank must run the same batches (one d_best exchange per batch)
+        bt = torch.tensor([batch], dtype=torch.int64, device="cuda")
+        torch.distributed.all_reduce(bt, op=torch.distributed.ReduceOp.MIN)
+        batch = int(bt.item())
     group = None
     hook = None
     if world > 1 and not args.no_exchange:

@@ -80,6 +80,13 @@ class ShardedSearch:
         from . import _lib
 
         hook = (lambda d: exchange_dbest(d, self.group)) if exchange else None
+        if batch is None:  # identical batching on every rank (one exchange per batch)
+            batch = self.index.auto_batch(params, advanced, len(queries))
+            bt = torch.tensor([batch], dtype=torch.int64, device=self.index.candidates.device)
+            import torch.distributed as dist
+
+            dist.all_reduce(bt, op=dist.ReduceOp.MIN, group=self.group)
+            batch = int(bt.item())
         res = self.index.search(queries, params, advanced=advanced, dim_range=dim_range, batch=batch,
                                 timing=timing, dbest_hook=hook, return_device=True)
         idx, dist_ = combine_results(res.best_index, res.best_distance, self.group)

@@ -306,3 +306,27 @@ def test_long_band_shapes(P, dt, n, d, w, pipe, monkeypatch):
     outs, _ = O.nn_search_batch(Qs.astype(np.float64), C.astype(np.float64), O.make_params(w, "lb_mv"), None, None)
     assert res.best_index.tolist() == [o.best_index for o in outs]
     assert res.best_distance.tolist() == [o.best_distance for o in outs]
+
+
+def test_tc_dtw_select_and_tune(P):
+    """Host logic over the GPU search (search.py:198-272): grid sizes, tie
+    rule, deterministic picks, and tuned parameters never change answers."""
+    rng = np.random.default_rng(5)
+    # clustered regime-switching series (synth.clustered_dataset's regime):
+    # box sets beat the single envelope box -> the clustering bound wins
+    centers = rng.normal(0, 8.0, (24, 2, 2))
+    state = (rng.random((24, 30)) < 0.35).cumsum(axis=1) % 2
+    series = np.take_along_axis(centers, state[:, :, None].repeat(2, 2), axis=1) + rng.normal(0, 0.25, (24, 30, 2))
+    queries, cands = list(series[:4]), list(series[4:])
+    params = P.SearchParams(window=5, method="tc_dtw")
+    assert P.tc_dtw_select(queries, cands, params) == P.Method.LB_PC
+    picks = {P.tc_dtw_select(queries[:1], cands[:1], params) for _ in range(3)}
+    assert len(picks) == 1
+    log = []
+    tuned = P.tune_params(queries, cands, params, seed=0, log=log)
+    assert len(log) == 7 and tuned.refresh_period == 5 and tuned.max_boxes == 6
+    base = [P.nn_search(q, cands, P.SearchParams(window=5, method="none")) for q in queries]
+    choice = P.tc_dtw_select(queries, cands, tuned)
+    for q, ref in zip(queries, base):
+        out = P.nn_search(q, cands, tuned, advanced=choice)
+        assert (out.best_index, out.best_distance) == (ref.best_index, ref.best_distance)
