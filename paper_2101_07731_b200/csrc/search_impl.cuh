@@ -1293,8 +1293,11 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = a.n, d = a.d, w = a.w, B = 2 * w + 1;
     const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T* qs = reinterpret_cast<T*>(smem_raw);                   // (n + 2w) * d
-    T* prow = qs + (size_t)(n + 2 * w) * d + (size_t)wib * B;  // per warp: B
+    // query rows with an odd word stride: consecutive lanes read consecutive
+    // columns without bank conflicts (fp64 d=8 was 16-way)
+    const int SP = (d % 2 == 1) ? d : d + 1;
+    T* qs = reinterpret_cast<T*>(smem_raw);                    // (n + 2w) * SP
+    T* prow = qs + (size_t)(n + 2 * w) * SP + (size_t)wib * B;  // per warp: B
     __shared__ int64_t tile_s;
     const T INF = dev_inf<T>();
     int64_t cached_q = -1;
@@ -1312,7 +1315,7 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
             for (int e = threadIdx.x; e < (n + 2 * w) * d; e += blockDim.x) {
                 const int r = e / d, p = e - (e / d) * d;
                 const int j = r - w;
-                qs[e] = (j >= 0 && j < n) ? qsrc[(int64_t)j * d + p] : INF;
+                qs[r * SP + p] = (j >= 0 && j < n) ? qsrc[(int64_t)j * d + p] : INF;
             }
             cached_q = q;
             __syncthreads();
@@ -1350,7 +1353,7 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
                             up = got;
                             dg = got_prev;
                         }
-                        const T* qp = qs + (size_t)(i + k) * d;
+                        const T* qp = qs + (size_t)(i + k) * SP;
                         T cost;
                         if constexpr (EXACT) {
                             cost = dist_exact<T, DMAX>(rp, qp, d);
@@ -2498,7 +2501,7 @@ static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tile
         kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
         return launch_status();
     }
-    const size_t smem = ((size_t)(p.n + 2 * p.w) * p.d + (size_t)8 * p.B) * sizeof(T);
+    const size_t smem = ((size_t)(p.n + 2 * p.w) * ((p.d % 2 == 1) ? p.d : p.d + 1) + (size_t)8 * p.B) * sizeof(T);
     auto kern = dtw_wave_kernel<T, DMAX, EXACT>;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
