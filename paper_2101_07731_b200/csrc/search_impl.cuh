@@ -523,28 +523,29 @@ __global__ void __launch_bounds__(256) compact_write_kernel(const T* __restrict_
 
 // per-(chunk, query) survivor segments -> tile counts; then fill
 static __global__ void seg_tiles_count_kernel(int64_t Q, int n_chunks, const int64_t* __restrict__ chunk_off,
-                                       int64_t* __restrict__ tile_cnt, int64_t* __restrict__ counters) {
+                                       int64_t* __restrict__ tile_cnt, int64_t* __restrict__ counters,
+                                       int tile_len = kTile) {
     const int64_t n_seg = Q * n_chunks;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_seg; g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t cnt = chunk_off[g + 1] - chunk_off[g];
-        tile_cnt[g] = (cnt + kTile - 1) / kTile;
-        if (cnt) atomicAdd(reinterpret_cast<unsigned long long*>(counters + (g % Q) * TCDTW_COUNTERS + TCDTW_C_SURVIVORS),
+        tile_cnt[g] = (cnt + tile_len - 1) / tile_len;
+        if (cnt && counters) atomicAdd(reinterpret_cast<unsigned long long*>(counters + (g % Q) * TCDTW_COUNTERS + TCDTW_C_SURVIVORS),
                            (unsigned long long)cnt);
     }
 }
 
 static __global__ void seg_tiles_fill_kernel(int64_t Q, int n_chunks, const int64_t* __restrict__ chunk_off,
-                                      const int64_t* __restrict__ tile_off, Tiles t) {
+                                      const int64_t* __restrict__ tile_off, Tiles t, int tile_len = kTile) {
     const int64_t n_seg = Q * n_chunks;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_seg; g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = chunk_off[g], e = chunk_off[g + 1];
         const int64_t t0 = tile_off[g];
-        const int64_t nt = (e - b + kTile - 1) / kTile;
+        const int64_t nt = (e - b + tile_len - 1) / tile_len;
         for (int64_t k = 0; k < nt; ++k) {
-            const int64_t bb = b + k * kTile;
+            const int64_t bb = b + k * tile_len;
             t.q[t0 + k] = (uint32_t)(g % Q);
             t.begin[t0 + k] = bb;
-            t.len[t0 + k] = (int32_t)((e - bb) < kTile ? (e - bb) : kTile);
+            t.len[t0 + k] = (int32_t)((e - bb) < tile_len ? (e - bb) : tile_len);
         }
     }
 }
@@ -575,6 +576,10 @@ struct SArgs {
     unsigned long long* done_cnt;
     int64_t done_cap;
     int refill_min;  // lane kernel: refill once at least this many lanes are free
+    // float32: queries as coordinate pairs with W INF columns before and
+    // W + 8 after, (Q, qpad_rows, (d+1)/2) float2 -- the lane4 ring's source
+    const float2* qpad;
+    int qpad_rows;
 };
 
 template <typename T>
@@ -1276,6 +1281,382 @@ static int launch_lane(const SArgs<T>& a, int d, int B, Tiles tl, int64_t n_tile
     }
     TCDTW_LANE_SPECS(TCDTW_LANE_CASE)
 #undef TCDTW_LANE_CASE
+    return TCDTW_NOT_SUPPORTED;
+}
+
+// ---------------------------- DTW, lane per pair, four rows per step (f32)
+// Float32 lane kernel for n % 4 == 0 and (2W+1) % 4 == 1.  A warp works on
+// ONE query at a time: it takes whole (chunk, query) survivor segments, and
+// the query (padded with W INF columns before and W+8 after) and its LB_MV
+// envelope sit in the warp's shared memory.  Each lane runs its own pair; a
+// step advances it by four DP rows i..i+3: iteration s reads query column
+// i - W + s once and applies it to all four rows (row r at band slot s - r),
+// so one window-point read serves four cells.  Row i+3's band replaces row
+// i-1's in place in a per-lane shared-memory row (row 0 reads slot s+1
+// while row 3 writes slot s-3); intermediate rows live in two registers
+// each, so the step is a rolled loop of 4-iteration blocks (small code).
+// Abandoning is tested on row i+3 only: row minima never decrease down the
+// matrix, so the last row of a step is the strongest test of the step.
+// Query columns are grouped by four with a two-word pad (8*DP + 2 words per
+// group, 16 distinct bank pairs for the lanes' row offsets i/4) and the
+// envelope by four rows with a one-float4 pad (8D + 4 words), so lanes on
+// different rows read shared memory with few conflicts.
+static __global__ void qpad_kernel(const float* __restrict__ q, int64_t Q, int n, int d, int w, int rows,
+                                   float2* __restrict__ out) {
+    const int DP = (d + 1) / 2;
+    const int64_t tot = Q * rows * DP;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int pp = (int)(e % DP);
+        const int64_t r = (e / DP) % rows, qi = e / ((int64_t)DP * rows);
+        const int64_t col = r - w;
+        float2 v = make_float2(dev_inf<float>(), dev_inf<float>());
+        if (col >= 0 && col < n) {
+            const float* src = q + (qi * n + col) * d;
+            v.x = src[2 * pp];
+            v.y = (2 * pp + 1 < d) ? src[2 * pp + 1] : 0.f;
+        }
+        out[e] = v;
+    }
+}
+
+template <int D>
+struct Lane4Layout {
+    static constexpr int DP = (D + 1) / 2;
+    static constexpr int QGS = 8 * DP + 2;  // words per 4-column query group
+    static constexpr int EGS = 8 * D + 4;   // words per 4-row envelope group (up rows, then lo rows)
+    // per-warp words: query groups, envelope groups, band row (B x 32 lanes)
+    __host__ __device__ static int q_words(int n, int w) { return ((n + 2 * w + 8) / 4 * QGS + 3) & ~3; }
+    __host__ __device__ static int e_words(int n) { return n / 4 * EGS; }
+    __host__ __device__ static int warp_words(int n, int w, int B) {
+        return q_words(n, w) + e_words(n) + B * 32;
+    }
+};
+
+template <int D, int B, bool CASC>
+__global__ void __launch_bounds__(64) dtw_lane4_kernel(SArgs<float> a, Tiles tl, int64_t n_tiles,
+                                                       const uint32_t* __restrict__ cand_of, float* __restrict__ res,
+                                                       int* __restrict__ tile_ctr) {
+    using L = Lane4Layout<D>;
+    constexpr int W = (B - 1) / 2, R = 4, DP = L::DP, QGS = L::QGS, EGS = L::EGS;
+    constexpr int NB = (B + R - 1) / R;  // 4-iteration blocks per step: prologue, NB-2 full, epilogue
+    static_assert(B % 4 == 1 && B >= 5, "band width 4m+1");
+    extern __shared__ __align__(16) float smem_f[];
+    const int n = a.n;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    float* const qs = smem_f + (size_t)wib * L::warp_words(n, a.w, B);  // query groups
+    float* const es = qs + L::q_words(n, a.w);                          // envelope groups
+    float* const ps = es + L::e_words(n) + lane;                        // band row: slot k at ps[k*32]
+    const unsigned FULL = 0xffffffffu;
+    const float INF = dev_inf<float>();
+    const bool casc = CASC && a.lb != nullptr && a.abandon && a.env_up != nullptr;
+    // warp-uniform work state: current tile, reservoir window, query in smem
+    int64_t t_begin = 0;
+    int t_q = -1, t_len = 0, t_next = 0, r_base = 0, slot_q = -1;
+    bool exhausted = false, have_tile = false;
+    float t_thr_raw = INF;
+    // reservoir: lane m holds entry r_base + m of the tile
+    uint32_t pf_c = 0;
+    float pf_lb = 0.f, pf_res = 0.f;
+    float pf_rows[4 * D];
+    // lane state
+    bool busy = false;
+    int64_t ent = 0;
+    int i = 0, since = 0;
+    const float* crow = nullptr;
+    float c[4 * D], nc[4 * D];
+    float thr = INF, thr_pend_raw = INF, lbtot = 0.f, prefix = 0.f;
+    int cq = -1;
+    long long c_comp = 0, c_ab = 0, c_cells = 0, c_issued = 0;
+    auto flush = [&]() {
+        if (cq >= 0) {
+            unsigned long long* ctr = reinterpret_cast<unsigned long long*>(a.counters + (int64_t)cq * TCDTW_COUNTERS);
+            if (c_comp) atomicAdd(ctr + TCDTW_C_DTW_COMPUTED, (unsigned long long)c_comp);
+            if (c_ab) atomicAdd(ctr + TCDTW_C_ABANDON_COUNT, (unsigned long long)c_ab);
+            if (c_cells) atomicAdd(ctr + TCDTW_C_DTW_CELLS, (unsigned long long)c_cells);
+            if (c_issued) atomicAdd(ctr + TCDTW_C_CELLS_ISSUED, (unsigned long long)c_issued);
+        }
+        c_comp = c_ab = c_cells = c_issued = 0;
+    };
+    auto load_rows = [&](float (&dst)[4 * D], const float* cr, int row) {  // rows row..row+3, row % 4 == 0
+        const float4* src = reinterpret_cast<const float4*>(cr + (int64_t)row * D);
+#pragma unroll
+        for (int v = 0; v < D; ++v) {
+            const float4 x = __ldg(src + v);
+            dst[4 * v] = x.x;
+            dst[4 * v + 1] = x.y;
+            dst[4 * v + 2] = x.z;
+            dst[4 * v + 3] = x.w;
+        }
+    };
+    auto load_reservoir = [&]() {  // entries r_base .. r_base+31 of the tile, one per lane
+        if (r_base + lane < t_len) {
+            const int64_t e = t_begin + r_base + lane;
+            pf_c = cand_of[e];
+            pf_res = res[e];
+            pf_lb = casc ? a.lb[(int64_t)t_q * a.N + pf_c] : 0.f;
+            load_rows(pf_rows, a.cands + (int64_t)pf_c * n * D, 0);
+        }
+        t_thr_raw = a.abandon ? load_volatile(a.dbest + t_q) : INF;
+    };
+    auto load_query = [&](int q) {  // the warp's query slot (all lanes idle)
+        __syncwarp();
+        const int qrows = a.qpad_rows;
+        const float2* src = a.qpad + (int64_t)q * qrows * DP;
+        for (int e = lane; e < qrows * DP; e += 32) {
+            const int col = e / DP, pp = e - (e / DP) * DP;
+            *reinterpret_cast<float2*>(qs + (col >> 2) * QGS + (col & 3) * 2 * DP + 2 * pp) = src[e];
+        }
+        if (casc) {
+            const float* eu = a.env_up + (int64_t)q * n * D;
+            const float* el = a.env_lo + (int64_t)q * n * D;
+            for (int e = lane; e < n * D; e += 32) {
+                const int row = e / D, p = e - (e / D) * D;
+                float* g = es + (row >> 2) * EGS + (row & 3) * D + p;
+                g[0] = eu[e];
+                g[4 * D] = el[e];
+            }
+        }
+        slot_q = q;
+        __syncwarp();
+    };
+    auto refill = [&]() {
+        unsigned freem = __ballot_sync(FULL, !busy);
+        if (__popc(freem) < a.refill_min && freem != FULL) return;
+        while (freem && !exhausted) {
+            if (!have_tile || t_next >= t_len) {
+                if (have_tile && t_next >= t_len) have_tile = false;
+                if (!have_tile) {
+                    int64_t tile = 0;
+                    if (lane == 0) tile = atomicAdd(tile_ctr, 1);
+                    tile = __shfl_sync(FULL, tile, 0);
+                    if (tile >= n_tiles) {
+                        exhausted = true;
+                        break;
+                    }
+                    t_q = (int)tl.q[tile];
+                    t_begin = tl.begin[tile];
+                    t_len = tl.len[tile];
+                    t_next = 0;
+                    r_base = 0;
+                    have_tile = true;
+                    load_reservoir();
+                }
+            }
+            if (t_q != slot_q) {
+                // the slot still serves busy lanes of the previous query: drain first
+                if (freem != FULL) return;
+                load_query(t_q);
+            }
+            if (t_next >= r_base + 32) {
+                r_base += 32;
+                load_reservoir();
+            }
+            const int avail = min(t_len, r_base + 32) - t_next;
+            const int take = min(avail, __popc(freem));
+            const int rank = __popc(freem & ((1u << lane) - 1u));
+            const int m = t_next - r_base + (rank < take ? rank : 0);
+            const uint32_t c_m = __shfl_sync(FULL, pf_c, m);
+            const float lb_m = __shfl_sync(FULL, pf_lb, m);
+            const float res_m = __shfl_sync(FULL, pf_res, m);
+            float r_m[4 * D];
+#pragma unroll
+            for (int u = 0; u < 4 * D; ++u) r_m[u] = __shfl_sync(FULL, pf_rows[u], m);
+            if (!busy && rank < take && !(res_m < 0.f)) {  // skip entries pruned by the advanced bound
+                if (t_q != cq) {
+                    flush();
+                    cq = t_q;
+                }
+                ent = t_begin + r_base + m;
+                crow = a.cands + (int64_t)c_m * n * D;
+                lbtot = lb_m;
+                prefix = 0.f;
+                thr = a.abandon ? scale_up<float>(t_thr_raw, a.mg.prune) : INF;
+                thr_pend_raw = t_thr_raw;
+#pragma unroll
+                for (int k = 0; k < B; ++k) ps[k * 32] = (k == W) ? 0.f : INF;
+#pragma unroll
+                for (int u = 0; u < 4 * D; ++u) c[u] = r_m[u];
+                i = 0;
+                since = 0;
+                busy = true;
+            }
+            t_next += take;
+            freem = __ballot_sync(FULL, !busy);
+        }
+    };
+    // one 4-iteration block of the step: iterations s = 4j + t, t = 0..3.
+    // MODE 0: prologue (row r starts at t = r), 1: all rows inside the band,
+    // 2: epilogue (s = B-1+t; row r leaves the band after t = r).
+    float cur[R], prv[R], pu = 0.f, rmin = INF;
+    auto block = [&](auto mode_tag, const float* qg, float* pk) {
+        constexpr int MODE = decltype(mode_tag)::value;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            float x[D];
+#pragma unroll
+            for (int pp = 0; pp < DP; ++pp) {
+                const float2 v = *reinterpret_cast<const float2*>(qg + t * 2 * DP + 2 * pp);
+                x[2 * pp] = v.x;
+                if (2 * pp + 1 < D) x[2 * pp + 1] = v.y;
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool active = MODE == 1 ? true : (MODE == 0 ? (r <= t) : (r >= t));
+                if (!active) {
+                    if (MODE == 2) {  // row r has left the band
+                        prv[r] = cur[r];
+                        cur[r] = INF;
+                    }
+                    continue;
+                }
+                float acc = 0.f;
+#pragma unroll
+                for (int p = 0; p < D; ++p) {
+                    const float df = c[r * D + p] - x[p];
+                    acc = fmaf(df, df, acc);
+                }
+                const float cost = fast_sqrt(acc);
+                float up, dg;
+                if (r == 0) {
+                    // slot k = s: up = band[s+1] (outside past slot B-1), diag = band[s]
+                    up = (MODE == 2) ? INF : pk[(t + 1) * 32];
+                    dg = pu;
+                    pu = up;
+                } else {
+                    up = cur[r - 1];
+                    dg = prv[r - 1];
+                }
+                const float v = cost + fminf(fminf(up, dg), cur[r]);
+                prv[r] = cur[r];
+                cur[r] = v;
+                if (r == R - 1) {
+                    pk[(t - 3) * 32] = v;  // slot s - 3
+                    rmin = fminf(rmin, v);
+                }
+            }
+        }
+    };
+    while (true) {
+        refill();
+        if (!__any_sync(FULL, busy) && exhausted) break;
+        c_issued += R * B;
+        if (busy) {
+            const bool more = i + R < n;
+            if (more) load_rows(nc, crow, i + R);  // consumed after the DP
+#pragma unroll
+            for (int r = 0; r < R; ++r) cur[r] = prv[r] = INF;
+            rmin = INF;
+            pu = ps[0];
+            const float* qg = qs + (i >> 2) * QGS;  // padded column i + s <-> query column i - W + s
+            float* pk = ps;                         // band slot 4j at pk
+            block(std::integral_constant<int, 0>{}, qg, pk);
+#pragma unroll 1
+            for (int j = 1; j < NB - 1; ++j) block(std::integral_constant<int, 1>{}, qg + j * QGS, pk + j * 4 * 32);
+            block(std::integral_constant<int, 2>{}, qg + (NB - 1) * QGS, pk + (NB - 1) * 4 * 32);
+            // cascade: LB_MV terms of rows i..i+3 from the envelope group
+            float bound = rmin;
+            if (casc) {
+                const float4* eg = reinterpret_cast<const float4*>(es + (i >> 2) * EGS);
+                float term[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) term[r] = 0.f;
+#pragma unroll
+                for (int v = 0; v < D; ++v) {
+                    const float4 u4 = eg[v], l4 = eg[D + v];
+                    const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int f = 4 * v + e, r = f / D;
+                        const float cv = c[f];
+                        const float dv = fmaxf(fmaxf(cv - uu[e], ll[e] - cv), 0.f);
+                        term[r] = fmaf(dv, dv, term[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) prefix += fast_sqrt(term[r]);
+                bound = rmin + fmaxf(lbtot * a.casc_lo - prefix * a.casc_hi, 0.f);
+            }
+            int stop = -1;
+            bool abandoned = false;
+            float fin = INF;
+            if (!more) {  // row i+3 is the last row
+                stop = n - 1;
+                fin = ps[W * 32];
+                abandoned = fin > thr;  // dtw.py:101-102
+            } else if (rmin > thr || bound > thr * a.casc_thr) {
+                stop = i + R - 1;
+                abandoned = true;
+            }
+            if (stop >= 0) {
+                res[ent] = abandoned ? INF : fin;
+                if (!abandoned) {
+                    atomic_min_nonneg<float>(a.dbest + cq, fin);
+                    note_done(a, cq, ent);
+                }
+                ++c_comp;
+                c_ab += abandoned ? 1 : 0;
+                c_cells += cells_upto(stop, n, W);
+                busy = false;
+            } else {
+                i += R;
+#pragma unroll
+                for (int u = 0; u < 4 * D; ++u) c[u] = nc[u];
+                since += R;
+                if (since >= 8) {
+                    since = 0;
+                    thr = scale_up<float>(thr_pend_raw, a.mg.prune);
+                    if (a.abandon) thr_pend_raw = load_volatile(a.dbest + cq);
+                }
+            }
+        }
+    }
+    flush();
+}
+
+#define TCDTW_LANE4_SPECS(X) \
+    X(3, 25) X(4, 25) X(5, 25) X(6, 25) X(8, 25) X(3, 13) X(4, 13) X(5, 13) X(6, 13) X(8, 13)
+
+static bool lane4_supported(const SArgs<float>& a, int d, int B) {
+    if (getenv("TCDTW_NO_LANE") || getenv("TCDTW_NO_LANE4")) return false;
+    if (a.n % 4 != 0 || a.qpad == nullptr || (reinterpret_cast<uintptr_t>(a.cands) % 16) != 0) return false;
+    bool ok = false;
+#define TCDTW_LANE4_OK(DD, BB) ok = ok || (d == DD && B == BB);
+    TCDTW_LANE4_SPECS(TCDTW_LANE4_OK)
+#undef TCDTW_LANE4_OK
+    return ok;
+}
+
+static int launch_lane4(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n_tiles, const uint32_t* cand_of,
+                        float* res, int* tctr, cudaStream_t st) {
+    constexpr int threads = 64;
+    if (!lane4_supported(a, d, B)) return TCDTW_NOT_SUPPORTED;
+    static const bool no_casc = getenv("TCDTW_NO_CASC") != nullptr;  // A/B switch for benchmarking
+    auto go = [&](auto kern, int words_per_warp) -> int {
+        const size_t smem = (size_t)(threads / 32) * words_per_warp * sizeof(float);
+        int dev = 0, sms = 148, occ = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (smem > 227 * 1024) return TCDTW_NOT_SUPPORTED;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return TCDTW_NOT_SUPPORTED;
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        if (occ < 1) return TCDTW_NOT_SUPPORTED;
+        int64_t grid = (int64_t)occ * sms;
+        const int64_t need = (n_tiles + 1) / 2;
+        if (grid > need) grid = need;
+        cudaMemsetAsync(tctr, 0, sizeof(int), st);
+        kern<<<(int)grid, threads, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
+        return launch_status();
+    };
+#define TCDTW_LANE4_CASE(DD, BB)                                                              \
+    if (d == DD && B == BB) {                                                                 \
+        const int ww = Lane4Layout<DD>::warp_words(a.n, a.w, BB);                             \
+        if (no_casc) return go(dtw_lane4_kernel<DD, BB, false>, ww);                          \
+        return go(dtw_lane4_kernel<DD, BB, true>, ww);                                        \
+    }
+    TCDTW_LANE4_SPECS(TCDTW_LANE4_CASE)
+#undef TCDTW_LANE4_CASE
     return TCDTW_NOT_SUPPORTED;
 }
 
@@ -2234,7 +2615,8 @@ struct Plan {
     int ub_ct, ub_stride;
     size_t o_up, o_lo, o_upT, o_loT, o_candT, o_steps, o_blo, o_bhi, o_bcnt, o_lb, o_seed, o_seedres,
         o_seedcnt, o_dbest, o_ccnt, o_coff, o_surv, o_res, o_tcnt, o_toff, o_tq, o_tb, o_tl, o_sq, o_sb, o_sl,
-        o_ctr, o_minv, o_min64, o_bidx, o_tctr, o_cub, o_fsc, o_tisc, total;
+        o_ctr, o_minv, o_min64, o_bidx, o_tctr, o_cub, o_fsc, o_tisc, o_qpad, total;
+    int qpad_rows;
     size_t cub_bytes;
     int fin_threads, adv_warps;
 };
@@ -2343,6 +2725,8 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     const bool ti = dsc->method == TCDTW_METHOD_LB_TI ||
                     (dsc->method == TCDTW_METHOD_TC_DTW && dsc->advanced == TCDTW_METHOD_LB_TI);
     p.o_tisc = take(ti ? (size_t)p.adv_warps * 32 * 3 * p.B * es : 0);
+    p.qpad_rows = p.n + 2 * p.w + 8;
+    p.o_qpad = take(p.exact ? 0 : (size_t)Q * p.qpad_rows * ((p.d + 1) / 2) * 8);
     p.total = o;
     return TCDTW_OK;
 }
@@ -2446,6 +2830,8 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
     a.done_list = nullptr;  // set for the survivors pass only
     a.done_cnt = nullptr;
     a.done_cap = 0;
+    a.qpad = p.exact ? nullptr : at<float2>(ws, p.o_qpad);
+    a.qpad_rows = p.qpad_rows;
     return a;
 }
 
@@ -2456,6 +2842,12 @@ static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tile
                       int* tctr, cudaStream_t st) {
     if (n_tiles <= 0) return TCDTW_OK;
     const bool no_lane = getenv("TCDTW_NO_LANE") != nullptr;  // A/B switch for benchmarking
+    if constexpr (!EXACT) {
+        if (!no_lane && getenv("TCDTW_NO_LANE4") == nullptr) {
+            const int s = launch_lane4(a, p.d, p.B, tl, n_tiles, cand_of, res, tctr, st);
+            if (s != TCDTW_NOT_SUPPORTED) return s;
+        }
+    }
     if (!no_lane) {
         const int s = launch_lane<T>(a, p.d, p.B, tl, n_tiles, cand_of, res, tctr, st);
         if (s != TCDTW_NOT_SUPPORTED) return s;
@@ -2534,6 +2926,13 @@ struct SearchImpl {
             TRY(planarize<T>(at<T>(ws, p.o_lo), p.Q, p.n * p.d, at<T>(ws, p.o_loT), st));
             TRY(planarize<T>((const T*)queries, p.Q, p.n * p.d, at<T>(ws, p.o_qT), st));
             TRY(planarize<T>((const T*)cands, p.N, p.n * p.d, at<T>(ws, p.o_candT), st));
+        }
+        if (!EXACT) {
+            const int DPq = (p.d + 1) / 2;
+            const int64_t tot = p.Q * p.qpad_rows * DPq;
+            qpad_kernel<<<grid_for(tot, 256), 256, 0, st>>>((const float*)queries, p.Q, p.n, p.d, p.w, p.qpad_rows,
+                                                             const_cast<float2*>(a.qpad));
+            TRY(launch_status());
         }
         if (a.adv == TCDTW_METHOD_LB_PC)
             TRY(series_box_sets(dtype, queries, p.Q, p.n, p.d, p.w, dsc->group_width, dsc->quant_levels, p.K,
@@ -2645,6 +3044,23 @@ struct SearchImpl {
             TRY(sa);
         }
         dbg_stage(st, "advanced");
+        if constexpr (!EXACT) {
+            // the lane4 kernel keeps one query per warp: hand it whole segments
+            if (n_tiles > 0 && lane4_supported(a, p.d, p.B)) {
+                seg_tiles_count_kernel<<<grid_for(n_seg, 256), 256, 0, st>>>(p.Q, p.n_chunks, coff, tcnt, nullptr,
+                                                                             (int)kChunk);
+                TRY(launch_status());
+                cb = p.cub_bytes;
+                if (cub::DeviceScan::ExclusiveSum(at<void>(ws, p.o_cub), cb, tcnt, toff, (int)(n_seg + 1), st) !=
+                    cudaSuccess)
+                    return TCDTW_CUDA_ERROR;
+                seg_tiles_fill_kernel<<<grid_for(n_seg, 128), 128, 0, st>>>(p.Q, p.n_chunks, coff, toff, tl,
+                                                                            (int)kChunk);
+                TRY(launch_status());
+                cudaMemcpyAsync(&n_tiles, toff + n_seg, 8, cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+            }
+        }
         tm.mark(6);
         unsigned long long* done_cnt = at<unsigned long long>(ws, p.o_done);
         unsigned long long* done_list = done_cnt + 8;
