@@ -1332,8 +1332,8 @@ struct Lane4Layout {
     }
 };
 
-template <int D, int B, bool CASC>
-__global__ void __launch_bounds__(64) dtw_lane4_kernel(SArgs<float> a, Tiles tl, int64_t n_tiles,
+template <int D, int B, bool CASC, bool PF, int MINB>
+__global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Tiles tl, int64_t n_tiles,
                                                        const uint32_t* __restrict__ cand_of, float* __restrict__ res,
                                                        int* __restrict__ tile_ctr) {
     using L = Lane4Layout<D>;
@@ -1357,7 +1357,7 @@ __global__ void __launch_bounds__(64) dtw_lane4_kernel(SArgs<float> a, Tiles tl,
     // reservoir: lane m holds entry r_base + m of the tile
     uint32_t pf_c = 0;
     float pf_lb = 0.f, pf_res = 0.f;
-    float pf_rows[4 * D];
+    float pf_rows[PF ? 4 * D : 1];
     // lane state
     bool busy = false;
     int64_t ent = 0;
@@ -1366,7 +1366,7 @@ __global__ void __launch_bounds__(64) dtw_lane4_kernel(SArgs<float> a, Tiles tl,
     float c[4 * D], nc[4 * D];
     float thr = INF, thr_pend_raw = INF, lbtot = 0.f, prefix = 0.f;
     int cq = -1;
-    long long c_comp = 0, c_ab = 0, c_cells = 0, c_issued = 0;
+    unsigned c_comp = 0, c_ab = 0, c_cells = 0, c_issued = 0;  // flushed before 2^31
     auto flush = [&]() {
         if (cq >= 0) {
             unsigned long long* ctr = reinterpret_cast<unsigned long long*>(a.counters + (int64_t)cq * TCDTW_COUNTERS);
@@ -1394,7 +1394,7 @@ __global__ void __launch_bounds__(64) dtw_lane4_kernel(SArgs<float> a, Tiles tl,
             pf_c = cand_of[e];
             pf_res = res[e];
             pf_lb = casc ? a.lb[(int64_t)t_q * a.N + pf_c] : 0.f;
-            load_rows(pf_rows, a.cands + (int64_t)pf_c * n * D, 0);
+            if constexpr (PF) load_rows(pf_rows, a.cands + (int64_t)pf_c * n * D, 0);
         }
         t_thr_raw = a.abandon ? load_volatile(a.dbest + t_q) : INF;
     };
@@ -1458,9 +1458,11 @@ __global__ void __launch_bounds__(64) dtw_lane4_kernel(SArgs<float> a, Tiles tl,
             const uint32_t c_m = __shfl_sync(FULL, pf_c, m);
             const float lb_m = __shfl_sync(FULL, pf_lb, m);
             const float res_m = __shfl_sync(FULL, pf_res, m);
-            float r_m[4 * D];
+            float r_m[PF ? 4 * D : 1];
+            if constexpr (PF) {
 #pragma unroll
-            for (int u = 0; u < 4 * D; ++u) r_m[u] = __shfl_sync(FULL, pf_rows[u], m);
+                for (int u = 0; u < 4 * D; ++u) r_m[u] = __shfl_sync(FULL, pf_rows[u], m);
+            }
             if (!busy && rank < take && !(res_m < 0.f)) {  // skip entries pruned by the advanced bound
                 if (t_q != cq) {
                     flush();
@@ -1474,8 +1476,12 @@ __global__ void __launch_bounds__(64) dtw_lane4_kernel(SArgs<float> a, Tiles tl,
                 thr_pend_raw = t_thr_raw;
 #pragma unroll
                 for (int k = 0; k < B; ++k) ps[k * 32] = (k == W) ? 0.f : INF;
+                if constexpr (PF) {
 #pragma unroll
-                for (int u = 0; u < 4 * D; ++u) c[u] = r_m[u];
+                    for (int u = 0; u < 4 * D; ++u) c[u] = r_m[u];
+                } else {
+                    load_rows(c, crow, 0);
+                }
                 i = 0;
                 since = 0;
                 busy = true;
@@ -1540,6 +1546,7 @@ __global__ void __launch_bounds__(64) dtw_lane4_kernel(SArgs<float> a, Tiles tl,
         refill();
         if (!__any_sync(FULL, busy) && exhausted) break;
         c_issued += R * B;
+        if (c_cells >= (1u << 30) || c_issued >= (1u << 30)) flush();
         if (busy) {
             const bool more = i + R < n;
             if (more) load_rows(nc, crow, i + R);  // consumed after the DP
@@ -1646,14 +1653,18 @@ static int launch_lane4(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n
         const int64_t need = (n_tiles + 1) / 2;
         if (grid > need) grid = need;
         cudaMemsetAsync(tctr, 0, sizeof(int), st);
-        kern<<<(int)grid, threads, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
+        SArgs<float> a4 = a;
+        if (!getenv("TCDTW_REFILL_MIN")) a4.refill_min = 4;
+        kern<<<(int)grid, threads, smem, st>>>(a4, tl, n_tiles, cand_of, res, tctr);
         return launch_status();
     };
+    // new pairs load their first rows themselves (no register prefetch in
+    // the reservoir): 126 registers at D=6, 16 warps per SM
 #define TCDTW_LANE4_CASE(DD, BB)                                                              \
     if (d == DD && B == BB) {                                                                 \
         const int ww = Lane4Layout<DD>::warp_words(a.n, a.w, BB);                             \
-        if (no_casc) return go(dtw_lane4_kernel<DD, BB, false>, ww);                          \
-        return go(dtw_lane4_kernel<DD, BB, true>, ww);                                        \
+        if (no_casc) return go(dtw_lane4_kernel<DD, BB, false, false, 8>, ww);                \
+        return go(dtw_lane4_kernel<DD, BB, true, false, 8>, ww);                              \
     }
     TCDTW_LANE4_SPECS(TCDTW_LANE4_CASE)
 #undef TCDTW_LANE4_CASE
