@@ -142,7 +142,23 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
                                                         const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                         int64_t Q, int64_t N, int n, int d, int TC,
                                                         T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
-                                                        int64_t c0);
+                                                        int64_t c0, bool v16);
+
+// asynchronous global -> shared copies; src_bytes < bytes zero-fills the rest
+__device__ __forceinline__ void cp_async_ca(void* dst, const void* src, int bytes, int src_bytes) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    if (bytes == 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(src), "r"(src_bytes) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_cg16(void* dst, const void* src, int src_bytes) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NPEND) : "memory"); }
 
 // DX > 0: the dimension count is a compile-time constant (fully unrolled
 // per-dimension loop for the hot shapes); DX == 0: runtime d.
@@ -150,7 +166,8 @@ template <typename T, int DMAX, bool EXACT, bool UB, int DX>
 __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ UT, const T* __restrict__ LT,
                                                           const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                           int64_t Q, int64_t N, int n, int d, int TC,
-                                                          T* __restrict__ out, T* __restrict__ ub_out, int ub_stride) {
+                                                          T* __restrict__ out, T* __restrict__ ub_out, int ub_stride,
+                                                          bool v16) {
     using Tile = MvTile<T, DMAX, EXACT>;
     constexpr int QT = Tile::QT, CTL = Tile::CT;
     // query tiles vary fastest: concurrently resident blocks share one
@@ -163,11 +180,12 @@ __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ 
     // candidate tile (block-uniform)
     if constexpr (UB) {
         if (((int64_t)blockIdx.x / nqt) % ub_stride != 0) {
-            lbmv_matrix_kernel_body<T, DMAX, EXACT, false, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0);
+            lbmv_matrix_kernel_body<T, DMAX, EXACT, false, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0,
+                                                               v16);
             return;
         }
     }
-    lbmv_matrix_kernel_body<T, DMAX, EXACT, UB, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0);
+    lbmv_matrix_kernel_body<T, DMAX, EXACT, UB, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0, v16);
 }
 
 template <typename T, int DMAX, bool EXACT, bool UB, int DX>
@@ -175,15 +193,60 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
                                                         const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                         int64_t Q, int64_t N, int n, int d, int TC,
                                                         T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
-                                                        int64_t c0) {
+                                                        int64_t c0, bool v16) {
     using Tile = MvTile<T, DMAX, EXACT>;
     constexpr int M = Tile::M, QT = Tile::QT, CTL = Tile::CT;
+    constexpr int VN = 16 / (int)sizeof(T);  // elements per 16-byte copy
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* us = reinterpret_cast<T*>(smem_raw);
-    T* ls = us + (size_t)TC * d * QT;
-    T* cs = ls + (size_t)TC * d * QT;
-    T* qs = cs + (size_t)TC * d * CTL;  // UB only
+    // two staging buffers (cp.async double buffering): round k+1's rows
+    // stream in while round k is consumed.  Buffer layout: us | ls | cs | qs
+    const size_t buf_elems = (size_t)TC * d * (3 * QT + CTL);
     const int tid = threadIdx.x;
+    auto stage = [&](int t0, int buf) {
+        T* us = reinterpret_cast<T*>(smem_raw) + buf * buf_elems;
+        T* ls = us + (size_t)TC * d * QT;
+        T* cs = ls + (size_t)TC * d * QT;
+        T* qs = cs + (size_t)TC * d * CTL;
+        const int tcn = (n - t0) < TC ? (n - t0) : TC;
+        const int rows = tcn * d;
+        const int64_t rbase = (int64_t)t0 * d;
+        if (v16) {
+            for (int e = tid * VN; e < rows * QT; e += 256 * VN) {
+                const int r = e / QT, qq = e - (e / QT) * QT;
+                const int64_t q = q0 + qq;
+                const int64_t left = Q - q;
+                const int sb = left <= 0 ? 0 : (left >= VN ? 16 : (int)left * (int)sizeof(T));
+                const int64_t off = (rbase + r) * Q + (sb ? q : 0);
+                cp_async_cg16(us + e, UT + off, sb);
+                cp_async_cg16(ls + e, LT + off, sb);
+                if constexpr (UB) cp_async_cg16(qs + e, QTP + off, sb);
+            }
+            for (int e = tid * VN; e < rows * CTL; e += 256 * VN) {
+                const int r = e / CTL, cc = e - (e / CTL) * CTL;
+                const int64_t c = c0 + cc;
+                const int64_t left = N - c;
+                const int sb = left <= 0 ? 0 : (left >= VN ? 16 : (int)left * (int)sizeof(T));
+                cp_async_cg16(cs + e, CT_ + (rbase + r) * N + (sb ? c : 0), sb);
+            }
+        } else {
+            for (int e = tid; e < rows * QT; e += 256) {
+                const int r = e / QT, qq = e - (e / QT) * QT;
+                const int64_t q = q0 + qq;
+                const int sb = q < Q ? (int)sizeof(T) : 0;
+                const int64_t off = (rbase + r) * Q + (sb ? q : 0);
+                cp_async_ca(us + e, UT + off, (int)sizeof(T), sb);
+                cp_async_ca(ls + e, LT + off, (int)sizeof(T), sb);
+                if constexpr (UB) cp_async_ca(qs + e, QTP + off, (int)sizeof(T), sb);
+            }
+            for (int e = tid; e < rows * CTL; e += 256) {
+                const int r = e / CTL, cc = e - (e / CTL) * CTL;
+                const int64_t c = c0 + cc;
+                const int sb = c < N ? (int)sizeof(T) : 0;
+                cp_async_ca(cs + e, CT_ + (rbase + r) * N + (sb ? c : 0), (int)sizeof(T), sb);
+            }
+        }
+        cp_async_commit();
+    };
     const int tq = tid & 15, tc = tid >> 4;
     T total[M][M], ubt[M][M];
 #pragma unroll
@@ -191,24 +254,21 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
 #pragma unroll
         for (int j = 0; j < M; ++j) total[i][j] = ubt[i][j] = T(0);
 
-    for (int t0 = 0; t0 < n; t0 += TC) {
+    stage(0, 0);
+    int buf = 0;
+    for (int t0 = 0; t0 < n; t0 += TC, buf ^= 1) {
         const int tcn = (n - t0) < TC ? (n - t0) : TC;
-        const int rows = tcn * d;
-        const int64_t rbase = (int64_t)t0 * d;
-        for (int e = tid; e < rows * QT; e += 256) {
-            const int r = e / QT, qq = e - (e / QT) * QT;
-            const int64_t q = q0 + qq;
-            const bool ok = q < Q;
-            us[e] = ok ? UT[(rbase + r) * Q + q] : T(0);
-            ls[e] = ok ? LT[(rbase + r) * Q + q] : T(0);
-            if constexpr (UB) qs[e] = ok ? QTP[(rbase + r) * Q + q] : T(0);
-        }
-        for (int e = tid; e < rows * CTL; e += 256) {
-            const int r = e / CTL, cc = e - (e / CTL) * CTL;
-            const int64_t c = c0 + cc;
-            cs[e] = c < N ? CT_[(rbase + r) * N + c] : T(0);
+        if (t0 + TC < n) {
+            stage(t0 + TC, buf ^ 1);  // the other buffer was released by the barrier closing the last round
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
+        const T* us = reinterpret_cast<const T*>(smem_raw) + buf * buf_elems;
+        const T* ls = us + (size_t)TC * d * QT;
+        const T* cs = ls + (size_t)TC * d * QT;
+        const T* qs = cs + (size_t)TC * d * CTL;
         for (int tt = 0; tt < tcn; ++tt) {
             if constexpr (EXACT) {
                 T sq[M][M][DMAX], sd[M][M][DMAX];
@@ -325,11 +385,16 @@ int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int6
                        T* out, T* ub_out, cudaStream_t st, int ub_stride = 1) {
     using Tile = MvTile<T, DMAX, EXACT>;
     const bool ub = ub_out != nullptr;
-    const size_t per_t = (size_t)d * ((ub ? 3 : 2) * Tile::QT + Tile::CT) * sizeof(T);
-    int TC = (int)((48 * 1024) / per_t);
+    // two staging buffers of TC time steps each (layout us | ls | cs | qs)
+    const size_t per_t = (size_t)d * (3 * Tile::QT + Tile::CT) * sizeof(T);
+    int TC = (int)((96 * 1024) / (2 * per_t));
     TC = TC < 1 ? 1 : (TC > 16 ? 16 : TC);
     TC = TC > n ? n : TC;
-    const size_t smem = per_t * TC;
+    const size_t smem = 2 * per_t * TC;
+    constexpr int VN = 16 / (int)sizeof(T);
+    const bool v16 = Q % VN == 0 && N % VN == 0 && (reinterpret_cast<uintptr_t>(UT) | reinterpret_cast<uintptr_t>(LT) |
+                                                     reinterpret_cast<uintptr_t>(QTP) | reinterpret_cast<uintptr_t>(CT)) % 16 == 0 &&
+                     (Tile::QT % VN) == 0 && (Tile::CT % VN) == 0;
     auto kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true, 0> : lbmv_matrix_kernel<T, DMAX, EXACT, false, 0>;
     if constexpr (!EXACT) {
 #define TCDTW_MV_DX(DD)                                                                                    \
@@ -347,7 +412,7 @@ int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int6
     const int64_t nct = (N + Tile::CT - 1) / Tile::CT;
     if (nqt * nct > 2147483647LL) return TCDTW_NOT_SUPPORTED;
     const unsigned grid = (unsigned)(nqt * nct);
-    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out, ub_stride);
+    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out, ub_stride, v16);
     return launch_status();
 }
 
@@ -2715,7 +2780,7 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     {
         const int64_t tiles = (N + p.ub_ct - 1) / p.ub_ct;
         int64_t st = tiles / 256;
-        p.ub_stride = (int)(st < 1 ? 1 : (st > 8 ? 8 : st));
+        p.ub_stride = (int)(st < 1 ? 1 : (st > 32 ? 32 : st));
         if (p.exact && p.d > 8) p.ub_ct = MvTile<double, 16, true>::CT;
         const int64_t full = (N / ((int64_t)p.ub_ct * p.ub_stride)) * p.ub_ct;
         const int64_t rem = N % ((int64_t)p.ub_ct * p.ub_stride);
