@@ -642,7 +642,7 @@ struct SArgs {
     int64_t done_cap;
     int refill_min;  // lane kernel: refill once at least this many lanes are free
     // float32: queries as coordinate pairs with W INF columns before and
-    // W + 8 after, (Q, qpad_rows, (d+1)/2) float2 -- the lane4 ring's source
+    // W + 8 after, (Q, qpad_rows, (d+1)/2) float2, staged by the R-row lane kernel
     const float2* qpad;
     int qpad_rows;
 };
@@ -1349,23 +1349,24 @@ static int launch_lane(const SArgs<T>& a, int d, int B, Tiles tl, int64_t n_tile
     return TCDTW_NOT_SUPPORTED;
 }
 
-// ---------------------------- DTW, lane per pair, four rows per step (f32)
-// Float32 lane kernel for n % 4 == 0 and (2W+1) % 4 == 1.  A warp works on
-// ONE query at a time: it takes whole (chunk, query) survivor segments, and
-// the query (padded with W INF columns before and W+8 after) and its LB_MV
-// envelope sit in the warp's shared memory.  Each lane runs its own pair; a
-// step advances it by four DP rows i..i+3: iteration s reads query column
-// i - W + s once and applies it to all four rows (row r at band slot s - r),
-// so one window-point read serves four cells.  Row i+3's band replaces row
-// i-1's in place in a per-lane shared-memory row (row 0 reads slot s+1
-// while row 3 writes slot s-3); intermediate rows live in two registers
-// each, so the step is a rolled loop of 4-iteration blocks (small code).
-// Abandoning is tested on row i+3 only: row minima never decrease down the
+// ------------------------- DTW, lane per pair, R rows per step (float32)
+// Float32 lane kernel for n % R == 0 (R = 4, or 2 for wide points).  A warp
+// works on ONE query at a time: it takes whole (chunk, query) survivor
+// segments, and the query (padded with W INF columns before and W+8 after)
+// and its LB_MV envelope sit in the warp's shared memory.  Each lane runs
+// its own pair; a step advances it by R DP rows i..i+R-1: iteration s reads
+// query column i - W + s once and applies it to all R rows (row r at band
+// slot s - r), so one window-point read serves R cells.  Row i+R-1's band
+// replaces row i-1's in place in a per-lane shared-memory row (row 0 reads
+// slot s+1 while row R-1 writes slot s-R+1); intermediate rows live in two
+// registers each, so the step is a rolled loop of R-iteration blocks with a
+// short unrolled prologue and tail (small code, no I-cache misses).
+// Abandoning is tested on row i+R-1 only: row minima never decrease down the
 // matrix, so the last row of a step is the strongest test of the step.
-// Query columns are grouped by four with a two-word pad (8*DP + 2 words per
-// group, 16 distinct bank pairs for the lanes' row offsets i/4) and the
-// envelope by four rows with a one-float4 pad (8D + 4 words), so lanes on
-// different rows read shared memory with few conflicts.
+// Query columns are grouped by R with a two-word pad (2R*DP + 2 words per
+// group: an odd number of 8-byte bank pairs) and the envelope by R rows with
+// a pad that makes the group an odd number of 16-byte bank quads, so lanes
+// on different rows read shared memory with few conflicts.
 static __global__ void qpad_kernel(const float* __restrict__ q, int64_t Q, int n, int d, int w, int rows,
                                    float2* __restrict__ out) {
     const int DP = (d + 1) / 2;
@@ -1384,33 +1385,35 @@ static __global__ void qpad_kernel(const float* __restrict__ q, int64_t Q, int n
     }
 }
 
-template <int D>
-struct Lane4Layout {
+template <int D, int R>
+struct LaneRLayout {
     static constexpr int DP = (D + 1) / 2;
-    static constexpr int QGS = 8 * DP + 2;  // words per 4-column query group
-    static constexpr int EGS = 8 * D + 4;   // words per 4-row envelope group (up rows, then lo rows)
-    // per-warp words: query groups, envelope groups, band row (B x 32 lanes)
-    __host__ __device__ static int q_words(int n, int w) { return ((n + 2 * w + 8) / 4 * QGS + 3) & ~3; }
-    __host__ __device__ static int e_words(int n) { return n / 4 * EGS; }
-    __host__ __device__ static int warp_words(int n, int w, int B) {
-        return q_words(n, w) + e_words(n) + B * 32;
-    }
+    static constexpr int QGS = 2 * R * DP + 2;  // words per R-column query group
+    static constexpr int EQ = R * D / 4;        // float4s per R-row envelope half (up or lo)
+    static constexpr int EGS = 8 * EQ + 4;      // words per R-row envelope group: 2*EQ + 1 (odd) float4s
+    static_assert((R * D) % 4 == 0, "R rows of D floats must be whole float4s");
+    __host__ __device__ static int q_words(int qrows) { return (((qrows + R - 1) / R) * QGS + 3) & ~3; }
+    __host__ __device__ static int e_words(int n) { return n / R * EGS; }
+    __host__ __device__ static int warp_words(int n, int qrows, int B) { return q_words(qrows) + e_words(n) + B * 32; }
 };
 
-template <int D, int B, bool CASC, bool PF, int MINB>
-__global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Tiles tl, int64_t n_tiles,
-                                                       const uint32_t* __restrict__ cand_of, float* __restrict__ res,
-                                                       int* __restrict__ tile_ctr) {
-    using L = Lane4Layout<D>;
-    constexpr int W = (B - 1) / 2, R = 4, DP = L::DP, QGS = L::QGS, EGS = L::EGS;
-    constexpr int NB = (B + R - 1) / R;  // 4-iteration blocks per step: prologue, NB-2 full, epilogue
-    static_assert(B % 4 == 1 && B >= 5, "band width 4m+1");
+template <int D, int B, int R, bool CASC, int MINB>
+__global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Tiles tl, int64_t n_tiles,
+                                                             const uint32_t* __restrict__ cand_of,
+                                                             float* __restrict__ res, int* __restrict__ tile_ctr) {
+    using L = LaneRLayout<D, R>;
+    constexpr int W = (B - 1) / 2, DP = L::DP, QGS = L::QGS, EGS = L::EGS, EQ = L::EQ, RD = R * D;
+    constexpr int NIT = B + R - 1;              // iterations per step
+    constexpr int JF = (B - 1 - R) / R;         // full blocks j = 1..JF (all rows inside the band)
+    constexpr int ST = R * (JF + 1);            // first tail iteration
+    static_assert(B >= R + 1 && JF >= 1, "band too narrow for R rows per step");
     extern __shared__ __align__(16) float smem_f[];
     const int n = a.n;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    float* const qs = smem_f + (size_t)wib * L::warp_words(n, a.w, B);  // query groups
-    float* const es = qs + L::q_words(n, a.w);                          // envelope groups
-    float* const ps = es + L::e_words(n) + lane;                        // band row: slot k at ps[k*32]
+    const int qrows = a.qpad_rows;
+    float* const qs = smem_f + (size_t)wib * L::warp_words(n, qrows, B);  // query groups
+    float* const es = qs + L::q_words(qrows);                              // envelope groups
+    float* const ps = es + L::e_words(n) + lane;                           // band row: slot k at ps[k*32]
     const unsigned FULL = 0xffffffffu;
     const float INF = dev_inf<float>();
     const bool casc = CASC && a.lb != nullptr && a.abandon && a.env_up != nullptr;
@@ -1422,13 +1425,12 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
     // reservoir: lane m holds entry r_base + m of the tile
     uint32_t pf_c = 0;
     float pf_lb = 0.f, pf_res = 0.f;
-    float pf_rows[PF ? 4 * D : 1];
     // lane state
     bool busy = false;
     int64_t ent = 0;
     int i = 0, since = 0;
     const float* crow = nullptr;
-    float c[4 * D], nc[4 * D];
+    float c[RD], nc[RD];
     float thr = INF, thr_pend_raw = INF, lbtot = 0.f, prefix = 0.f;
     int cq = -1;
     unsigned c_comp = 0, c_ab = 0, c_cells = 0, c_issued = 0;  // flushed before 2^31
@@ -1442,10 +1444,10 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
         }
         c_comp = c_ab = c_cells = c_issued = 0;
     };
-    auto load_rows = [&](float (&dst)[4 * D], const float* cr, int row) {  // rows row..row+3, row % 4 == 0
+    auto load_rows = [&](float (&dst)[RD], const float* cr, int row) {  // rows row..row+R-1, row % R == 0
         const float4* src = reinterpret_cast<const float4*>(cr + (int64_t)row * D);
 #pragma unroll
-        for (int v = 0; v < D; ++v) {
+        for (int v = 0; v < RD / 4; ++v) {
             const float4 x = __ldg(src + v);
             dst[4 * v] = x.x;
             dst[4 * v + 1] = x.y;
@@ -1459,26 +1461,24 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
             pf_c = cand_of[e];
             pf_res = res[e];
             pf_lb = casc ? a.lb[(int64_t)t_q * a.N + pf_c] : 0.f;
-            if constexpr (PF) load_rows(pf_rows, a.cands + (int64_t)pf_c * n * D, 0);
         }
         t_thr_raw = a.abandon ? load_volatile(a.dbest + t_q) : INF;
     };
     auto load_query = [&](int q) {  // the warp's query slot (all lanes idle)
         __syncwarp();
-        const int qrows = a.qpad_rows;
         const float2* src = a.qpad + (int64_t)q * qrows * DP;
         for (int e = lane; e < qrows * DP; e += 32) {
             const int col = e / DP, pp = e - (e / DP) * DP;
-            *reinterpret_cast<float2*>(qs + (col >> 2) * QGS + (col & 3) * 2 * DP + 2 * pp) = src[e];
+            *reinterpret_cast<float2*>(qs + (col / R) * QGS + (col % R) * 2 * DP + 2 * pp) = src[e];
         }
         if (casc) {
             const float* eu = a.env_up + (int64_t)q * n * D;
             const float* el = a.env_lo + (int64_t)q * n * D;
             for (int e = lane; e < n * D; e += 32) {
                 const int row = e / D, p = e - (e / D) * D;
-                float* g = es + (row >> 2) * EGS + (row & 3) * D + p;
+                float* g = es + (row / R) * EGS + (row % R) * D + p;
                 g[0] = eu[e];
-                g[4 * D] = el[e];
+                g[4 * EQ] = el[e];
             }
         }
         slot_q = q;
@@ -1489,23 +1489,21 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
         if (__popc(freem) < a.refill_min && freem != FULL) return;
         while (freem && !exhausted) {
             if (!have_tile || t_next >= t_len) {
-                if (have_tile && t_next >= t_len) have_tile = false;
-                if (!have_tile) {
-                    int64_t tile = 0;
-                    if (lane == 0) tile = atomicAdd(tile_ctr, 1);
-                    tile = __shfl_sync(FULL, tile, 0);
-                    if (tile >= n_tiles) {
-                        exhausted = true;
-                        break;
-                    }
-                    t_q = (int)tl.q[tile];
-                    t_begin = tl.begin[tile];
-                    t_len = tl.len[tile];
-                    t_next = 0;
-                    r_base = 0;
-                    have_tile = true;
-                    load_reservoir();
+                have_tile = false;
+                int64_t tile = 0;
+                if (lane == 0) tile = atomicAdd(tile_ctr, 1);
+                tile = __shfl_sync(FULL, tile, 0);
+                if (tile >= n_tiles) {
+                    exhausted = true;
+                    break;
                 }
+                t_q = (int)tl.q[tile];
+                t_begin = tl.begin[tile];
+                t_len = tl.len[tile];
+                t_next = 0;
+                r_base = 0;
+                have_tile = true;
+                load_reservoir();
             }
             if (t_q != slot_q) {
                 // the slot still serves busy lanes of the previous query: drain first
@@ -1523,11 +1521,6 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
             const uint32_t c_m = __shfl_sync(FULL, pf_c, m);
             const float lb_m = __shfl_sync(FULL, pf_lb, m);
             const float res_m = __shfl_sync(FULL, pf_res, m);
-            float r_m[PF ? 4 * D : 1];
-            if constexpr (PF) {
-#pragma unroll
-                for (int u = 0; u < 4 * D; ++u) r_m[u] = __shfl_sync(FULL, pf_rows[u], m);
-            }
             if (!busy && rank < take && !(res_m < 0.f)) {  // skip entries pruned by the advanced bound
                 if (t_q != cq) {
                     flush();
@@ -1541,12 +1534,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
                 thr_pend_raw = t_thr_raw;
 #pragma unroll
                 for (int k = 0; k < B; ++k) ps[k * 32] = (k == W) ? 0.f : INF;
-                if constexpr (PF) {
-#pragma unroll
-                    for (int u = 0; u < 4 * D; ++u) c[u] = r_m[u];
-                } else {
-                    load_rows(c, crow, 0);
-                }
+                load_rows(c, crow, 0);
                 i = 0;
                 since = 0;
                 busy = true;
@@ -1555,55 +1543,49 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
             freem = __ballot_sync(FULL, !busy);
         }
     };
-    // one 4-iteration block of the step: iterations s = 4j + t, t = 0..3.
-    // MODE 0: prologue (row r starts at t = r), 1: all rows inside the band,
-    // 2: epilogue (s = B-1+t; row r leaves the band after t = r).
     float cur[R], prv[R], pu = 0.f, rmin = INF;
-    auto block = [&](auto mode_tag, const float* qg, float* pk) {
-        constexpr int MODE = decltype(mode_tag)::value;
+    // iteration s of the step: window column i - W + s for rows i..i+R-1.
+    // qx: the column's 2*DP words; pk: band slot s.  With `full`, every row is
+    // inside the band and row 0's upper neighbour (slot s+1) exists; otherwise
+    // s is a compile-time constant after unrolling and the checks fold.
+    auto iter = [&](int s, bool full, const float* qx, float* pk) {
+        float x[D];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            float x[D];
+        for (int pp = 0; pp < DP; ++pp) {
+            const float2 v = *reinterpret_cast<const float2*>(qx + 2 * pp);
+            x[2 * pp] = v.x;
+            if (2 * pp + 1 < D) x[2 * pp + 1] = v.y;
+        }
 #pragma unroll
-            for (int pp = 0; pp < DP; ++pp) {
-                const float2 v = *reinterpret_cast<const float2*>(qg + t * 2 * DP + 2 * pp);
-                x[2 * pp] = v.x;
-                if (2 * pp + 1 < D) x[2 * pp + 1] = v.y;
-            }
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const bool active = MODE == 1 ? true : (MODE == 0 ? (r <= t) : (r >= t));
-                if (!active) {
-                    if (MODE == 2) {  // row r has left the band
-                        prv[r] = cur[r];
-                        cur[r] = INF;
-                    }
-                    continue;
-                }
-                float acc = 0.f;
-#pragma unroll
-                for (int p = 0; p < D; ++p) {
-                    const float df = c[r * D + p] - x[p];
-                    acc = fmaf(df, df, acc);
-                }
-                const float cost = fast_sqrt(acc);
-                float up, dg;
-                if (r == 0) {
-                    // slot k = s: up = band[s+1] (outside past slot B-1), diag = band[s]
-                    up = (MODE == 2) ? INF : pk[(t + 1) * 32];
-                    dg = pu;
-                    pu = up;
-                } else {
-                    up = cur[r - 1];
-                    dg = prv[r - 1];
-                }
-                const float v = cost + fminf(fminf(up, dg), cur[r]);
+        for (int r = 0; r < R; ++r) {
+            const bool active = full || (s - r >= 0 && s - r <= B - 1);
+            if (!active) {  // not started (all INF) or past slot B-1
                 prv[r] = cur[r];
-                cur[r] = v;
-                if (r == R - 1) {
-                    pk[(t - 3) * 32] = v;  // slot s - 3
-                    rmin = fminf(rmin, v);
-                }
+                cur[r] = INF;
+                continue;
+            }
+            float acc = 0.f;
+#pragma unroll
+            for (int p = 0; p < D; ++p) {
+                const float df = c[r * D + p] - x[p];
+                acc = fmaf(df, df, acc);
+            }
+            const float cost = fast_sqrt(acc);
+            float up, dg;
+            if (r == 0) {
+                up = (full || s + 1 <= B - 1) ? pk[32] : INF;
+                dg = pu;
+                pu = up;
+            } else {
+                up = cur[r - 1];
+                dg = prv[r - 1];
+            }
+            const float v = cost + fminf(fminf(up, dg), cur[r]);
+            prv[r] = cur[r];
+            cur[r] = v;
+            if (r == R - 1) {
+                pk[(1 - R) * 32] = v;  // slot s - R + 1
+                rmin = fminf(rmin, v);
             }
         }
     };
@@ -1619,22 +1601,28 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
             for (int r = 0; r < R; ++r) cur[r] = prv[r] = INF;
             rmin = INF;
             pu = ps[0];
-            const float* qg = qs + (i >> 2) * QGS;  // padded column i + s <-> query column i - W + s
-            float* pk = ps;                         // band slot 4j at pk
-            block(std::integral_constant<int, 0>{}, qg, pk);
+            const float* qg = qs + (i / R) * QGS;  // padded column i + s <-> query column i - W + s
+#pragma unroll
+            for (int s = 0; s < R; ++s) iter(s, false, qg + s * 2 * DP, ps + s * 32);
 #pragma unroll 1
-            for (int j = 1; j < NB - 1; ++j) block(std::integral_constant<int, 1>{}, qg + j * QGS, pk + j * 4 * 32);
-            block(std::integral_constant<int, 2>{}, qg + (NB - 1) * QGS, pk + (NB - 1) * 4 * 32);
-            // cascade: LB_MV terms of rows i..i+3 from the envelope group
+            for (int j = 1; j <= JF; ++j) {
+                const float* qb = qg + j * QGS;
+                float* pb = ps + j * R * 32;
+#pragma unroll
+                for (int t = 0; t < R; ++t) iter(j * R + t, true, qb + t * 2 * DP, pb + t * 32);
+            }
+#pragma unroll
+            for (int s = ST; s < NIT; ++s) iter(s, false, qg + (s / R) * QGS + (s % R) * 2 * DP, ps + s * 32);
+            // cascade: LB_MV terms of rows i..i+R-1 from the envelope group
             float bound = rmin;
             if (casc) {
-                const float4* eg = reinterpret_cast<const float4*>(es + (i >> 2) * EGS);
+                const float4* eg = reinterpret_cast<const float4*>(es + (i / R) * EGS);
                 float term[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) term[r] = 0.f;
 #pragma unroll
-                for (int v = 0; v < D; ++v) {
-                    const float4 u4 = eg[v], l4 = eg[D + v];
+                for (int v = 0; v < EQ; ++v) {
+                    const float4 u4 = eg[v], l4 = eg[EQ + v];
                     const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -1651,7 +1639,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
             int stop = -1;
             bool abandoned = false;
             float fin = INF;
-            if (!more) {  // row i+3 is the last row
+            if (!more) {  // row i+R-1 is the last row
                 stop = n - 1;
                 fin = ps[W * 32];
                 abandoned = fin > thr;  // dtw.py:101-102
@@ -1672,7 +1660,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
             } else {
                 i += R;
 #pragma unroll
-                for (int u = 0; u < 4 * D; ++u) c[u] = nc[u];
+                for (int u = 0; u < RD; ++u) c[u] = nc[u];
                 since += R;
                 if (since >= 8) {
                     since = 0;
@@ -1685,23 +1673,26 @@ __global__ void __launch_bounds__(64, MINB) dtw_lane4_kernel(SArgs<float> a, Til
     flush();
 }
 
-#define TCDTW_LANE4_SPECS(X) \
-    X(3, 25) X(4, 25) X(5, 25) X(6, 25) X(8, 25) X(3, 13) X(4, 13) X(5, 13) X(6, 13) X(8, 13)
+// (d, 2W+1, rows per step) shapes served by dtw_laner_kernel
+#define TCDTW_LANER_SPECS(X)                                                                          \
+    X(3, 25, 4) X(4, 25, 4) X(5, 25, 4) X(6, 25, 4) X(8, 25, 4) X(3, 13, 4) X(4, 13, 4) X(5, 13, 4) \
+    X(6, 13, 4) X(8, 13, 4) X(20, 13, 2) X(5, 103, 4)
 
-static bool lane4_supported(const SArgs<float>& a, int d, int B) {
-    if (getenv("TCDTW_NO_LANE") || getenv("TCDTW_NO_LANE4")) return false;
-    if (a.n % 4 != 0 || a.qpad == nullptr || (reinterpret_cast<uintptr_t>(a.cands) % 16) != 0) return false;
-    bool ok = false;
-#define TCDTW_LANE4_OK(DD, BB) ok = ok || (d == DD && B == BB);
-    TCDTW_LANE4_SPECS(TCDTW_LANE4_OK)
-#undef TCDTW_LANE4_OK
-    return ok;
+static int laner_rows(const SArgs<float>& a, int d, int B) {  // rows per step, 0 = not served
+    if (getenv("TCDTW_NO_LANE") || getenv("TCDTW_NO_LANE4")) return 0;
+    if (a.qpad == nullptr || (reinterpret_cast<uintptr_t>(a.cands) % 16) != 0) return 0;
+    int rows = 0;
+#define TCDTW_LANER_OK(DD, BB, RR) \
+    if (d == DD && B == BB && a.n % RR == 0) rows = RR;
+    TCDTW_LANER_SPECS(TCDTW_LANER_OK)
+#undef TCDTW_LANER_OK
+    return rows;
 }
 
-static int launch_lane4(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n_tiles, const uint32_t* cand_of,
+static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n_tiles, const uint32_t* cand_of,
                         float* res, int* tctr, cudaStream_t st) {
     constexpr int threads = 64;
-    if (!lane4_supported(a, d, B)) return TCDTW_NOT_SUPPORTED;
+    if (laner_rows(a, d, B) == 0) return TCDTW_NOT_SUPPORTED;
     static const bool no_casc = getenv("TCDTW_NO_CASC") != nullptr;  // A/B switch for benchmarking
     auto go = [&](auto kern, int words_per_warp) -> int {
         const size_t smem = (size_t)(threads / 32) * words_per_warp * sizeof(float);
@@ -1724,15 +1715,15 @@ static int launch_lane4(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n
         return launch_status();
     };
     // new pairs load their first rows themselves (no register prefetch in
-    // the reservoir): 126 registers at D=6, 16 warps per SM
-#define TCDTW_LANE4_CASE(DD, BB)                                                              \
-    if (d == DD && B == BB) {                                                                 \
-        const int ww = Lane4Layout<DD>::warp_words(a.n, a.w, BB);                             \
-        if (no_casc) return go(dtw_lane4_kernel<DD, BB, false, false, 8>, ww);                \
-        return go(dtw_lane4_kernel<DD, BB, true, false, 8>, ww);                              \
+    // the reservoir): 126 registers at d=6, 16 warps per SM
+#define TCDTW_LANER_CASE(DD, BB, RR)                                                          \
+    if (d == DD && B == BB && a.n % RR == 0) {                                                \
+        const int ww = LaneRLayout<DD, RR>::warp_words(a.n, a.qpad_rows, BB);                 \
+        if (no_casc) return go(dtw_laner_kernel<DD, BB, RR, false, 8>, ww);                   \
+        return go(dtw_laner_kernel<DD, BB, RR, true, 8>, ww);                                 \
     }
-    TCDTW_LANE4_SPECS(TCDTW_LANE4_CASE)
-#undef TCDTW_LANE4_CASE
+    TCDTW_LANER_SPECS(TCDTW_LANER_CASE)
+#undef TCDTW_LANER_CASE
     return TCDTW_NOT_SUPPORTED;
 }
 
@@ -2920,7 +2911,7 @@ static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tile
     const bool no_lane = getenv("TCDTW_NO_LANE") != nullptr;  // A/B switch for benchmarking
     if constexpr (!EXACT) {
         if (!no_lane && getenv("TCDTW_NO_LANE4") == nullptr) {
-            const int s = launch_lane4(a, p.d, p.B, tl, n_tiles, cand_of, res, tctr, st);
+            const int s = launch_laner(a, p.d, p.B, tl, n_tiles, cand_of, res, tctr, st);
             if (s != TCDTW_NOT_SUPPORTED) return s;
         }
     }
@@ -3121,8 +3112,8 @@ struct SearchImpl {
         }
         dbg_stage(st, "advanced");
         if constexpr (!EXACT) {
-            // the lane4 kernel keeps one query per warp: hand it whole segments
-            if (n_tiles > 0 && lane4_supported(a, p.d, p.B)) {
+            // the R-row lane kernel keeps one query per warp: hand it whole segments
+            if (n_tiles > 0 && laner_rows(a, p.d, p.B) > 0) {
                 seg_tiles_count_kernel<<<grid_for(n_seg, 256), 256, 0, st>>>(p.Q, p.n_chunks, coff, tcnt, nullptr,
                                                                              (int)kChunk);
                 TRY(launch_status());
