@@ -337,13 +337,15 @@ def run_ours(args):
         ph = dict(zip(_lib.PHASES, pv.tolist()))
 
     # ALU issue-rate probe (FP32 FFMA, independent chains) on this box
-    sink = torch.empty(1, device="cuda")
     lane_ops = __import__("ctypes").c_double()
-    L.tcdtw_alu_probe(0, 148 * 8, 2000, sink.data_ptr(), __import__("ctypes").byref(lane_ops),
+    # the DTW arithmetic type's FMA rate (FP64 issues at half the FP32 rate)
+    probe_dt = 1 if wl.dtype == "f64" else 0
+    sink = torch.empty(1, device="cuda", dtype=torch.float64)
+    L.tcdtw_alu_probe(probe_dt, 148 * 8, 2000, sink.data_ptr(), __import__("ctypes").byref(lane_ops),
                       _lib.stream_ptr())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    L.tcdtw_alu_probe(0, 148 * 8, 2000, sink.data_ptr(), __import__("ctypes").byref(lane_ops),
+    L.tcdtw_alu_probe(probe_dt, 148 * 8, 2000, sink.data_ptr(), __import__("ctypes").byref(lane_ops),
                       _lib.stream_ptr())
     e1.record()
     torch.cuda.synchronize()
@@ -368,12 +370,13 @@ def run_ours(args):
     else:
         ops = dtw_cells * (2 * d + 4)
         achieved = ops / (dtw_ms / 1e3) / 1e12
-        roof = {"kernel": "dtw_lane_kernel", "bound": "alu", "achieved": achieved, "peak": alu_peak,
+        roof = {"kernel": index.dtw_kernel(params, advanced, batch), "bound": "alu", "achieved": achieved, "peak": alu_peak,
                 "unit": "Tlane-op/s", "frac": achieved / alu_peak, "traffic": traffic_from_profile(dtw_cells / max(1, -(-n_q // batch))),
                 "algorithmic_ops": f"(2d+4) = {2 * d + 4} per DP cell x {dtw_cells:.4g} cells (SURVEY 8d)"}
-    roof["peak_source"] = ("tcdtw_alu_probe FFMA issue rate measured in this run (nominal 148 SM x 128 lanes x "
-                           f"{measured_peaks().get('sm_max_mhz', 1965)} MHz = "
-                           f"{148 * 128 * measured_peaks().get('sm_max_mhz', 1965) / 1e6:.1f} T)")
+    lanes = 64 if wl.dtype == "f64" else 128
+    roof["peak_source"] = (f"tcdtw_alu_probe {'DFMA' if wl.dtype == 'f64' else 'FFMA'} issue rate measured in this "
+                           f"run (nominal 148 SM x {lanes} lanes x {measured_peaks().get('sm_max_mhz', 1965)} MHz = "
+                           f"{148 * lanes * measured_peaks().get('sm_max_mhz', 1965) / 1e6:.1f} T)")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -199,6 +199,10 @@ int tcdtw_lb_mv_matrix(int dtype, const void *upper, const void *lower, const vo
                        int64_t n_queries, int64_t n_candidates, int32_t n, int32_t dims, void *out,
                        void *stream);
 
+/* Name of the DTW kernel the survivors pass launches for this shape
+ * (informational; a static string). */
+const char *tcdtw_dtw_kernel_name(const tcdtw_search_desc *desc);
+
 /* Issue-rate probe: a dependent-chain-free FFMA/DFMA loop, for measuring
  * the ALU roofline on the box.  Returns lane-operations issued. */
 int tcdtw_alu_probe(int dtype, int32_t blocks, int32_t iters, void *sink, double *lane_ops,

@@ -33,6 +33,7 @@ int search_finish(const tcdtw_search_desc*, const void*, const void*, const void
                   int64_t*, double*, int64_t*, cudaStream_t);
 int lb_mv_matrix(int, const void*, const void*, const void*, int64_t, int64_t, int, int, void*, cudaStream_t);
 int alu_probe(int, int, int, void*, double*, cudaStream_t);
+const char* dtw_kernel_name(const tcdtw_search_desc*);
 }  // namespace tcdtw
 
 using namespace tcdtw;
@@ -177,6 +178,11 @@ int tcdtw_lb_mv_matrix(int dtype, const void* upper, const void* lower, const vo
         return TCDTW_INVALID_INPUT;
     if (!upper || !lower || !candidates || !out) return TCDTW_INVALID_INPUT;
     return lb_mv_matrix(dtype, upper, lower, candidates, n_queries, n_candidates, n, dims, out, S(stream));
+}
+
+const char* tcdtw_dtw_kernel_name(const tcdtw_search_desc* desc) {
+    if (!desc) return "invalid";
+    return dtw_kernel_name(desc);
 }
 
 int tcdtw_alu_probe(int dtype, int32_t blocks, int32_t iters, void* sink, double* lane_ops, void* stream) {

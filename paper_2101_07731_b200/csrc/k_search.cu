@@ -55,6 +55,28 @@ int lb_mv_matrix(int dtype, const void* up, const void* lo, const void* cands, i
     return TCDTW_INVALID_INPUT;
 }
 
+// Which DTW kernel the survivors pass runs for this shape (launch_dtw's
+// order; assumes 16-byte aligned candidates).
+const char* dtw_kernel_name(const tcdtw_search_desc* dsc) {
+    Plan p;
+    if (make_plan(dsc, &p) != TCDTW_OK) return "invalid";
+    if (getenv("TCDTW_NO_LANE") == nullptr) {
+        if (!p.exact) {
+            const int r = laner_rows_shape(p.n, p.d, p.B);
+            if (r == 4) return "dtw_laner_kernel<R=4>";
+            if (r == 2) return "dtw_laner_kernel<R=2>";
+        }
+        bool lane = false;
+#define TCDTW_NAME_CASE(TT, DD, BB) lane = lane || ((sizeof(TT) == 8) == p.exact && p.d == DD && p.B == BB);
+        TCDTW_LANE_SPECS(TCDTW_NAME_CASE)
+#undef TCDTW_NAME_CASE
+        if (lane) return "dtw_lane_kernel";
+    }
+    if (p.B <= 64) return "dtw_tpp_kernel";
+    if (getenv("TCDTW_PIPE") && p.w >= 32) return "dtw_pipe_kernel";
+    return "dtw_wave_kernel";
+}
+
 int alu_probe(int dtype, int blocks, int iters, void* sink, double* lane_ops, cudaStream_t st) {
     if (dtype == TCDTW_F64) alu_probe_kernel<double><<<blocks, 256, 0, st>>>(iters, (double*)sink);
     else alu_probe_kernel<float><<<blocks, 256, 0, st>>>(iters, (float*)sink);

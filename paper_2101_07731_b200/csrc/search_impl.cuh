@@ -1678,15 +1678,19 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     X(3, 25, 4) X(4, 25, 4) X(5, 25, 4) X(6, 25, 4) X(8, 25, 4) X(3, 13, 4) X(4, 13, 4) X(5, 13, 4) \
     X(6, 13, 4) X(8, 13, 4) X(20, 13, 2) X(5, 103, 4)
 
-static int laner_rows(const SArgs<float>& a, int d, int B) {  // rows per step, 0 = not served
+static int laner_rows_shape(int n, int d, int B) {  // rows per step for this shape, 0 = not served
     if (getenv("TCDTW_NO_LANE") || getenv("TCDTW_NO_LANE4")) return 0;
-    if (a.qpad == nullptr || (reinterpret_cast<uintptr_t>(a.cands) % 16) != 0) return 0;
     int rows = 0;
 #define TCDTW_LANER_OK(DD, BB, RR) \
-    if (d == DD && B == BB && a.n % RR == 0) rows = RR;
+    if (d == DD && B == BB && n % RR == 0) rows = RR;
     TCDTW_LANER_SPECS(TCDTW_LANER_OK)
 #undef TCDTW_LANER_OK
     return rows;
+}
+
+static int laner_rows(const SArgs<float>& a, int d, int B) {
+    if (a.qpad == nullptr || (reinterpret_cast<uintptr_t>(a.cands) % 16) != 0) return 0;
+    return laner_rows_shape(a.n, d, B);
 }
 
 static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n_tiles, const uint32_t* cand_of,

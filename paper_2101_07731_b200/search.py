@@ -166,6 +166,12 @@ class SearchIndex:
                    "workspace_size")
         return int(out.value)
 
+    def dtw_kernel(self, params: SearchParams, advanced=None, n_q: int = 1) -> str:
+        """Name of the DTW kernel the survivors pass launches for this shape."""
+        adv = _advanced_method(params, advanced)
+        desc = self._desc(params, adv, n_q, 0, False, None)
+        return _lib.load_library().tcdtw_dtw_kernel_name(ctypes.byref(desc)).decode()
+
     def auto_batch(self, params: SearchParams, advanced=None, n_q: int = 1, budget_bytes: int | None = None,
                    seeds: int = 0) -> int:
         """Largest query batch whose workspace fits the budget (default:
