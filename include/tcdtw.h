@@ -149,9 +149,20 @@ typedef struct tcdtw_search_desc {
     int32_t seeds;          /* seed DTWs per query (0 = default 8) */
     int32_t flags;          /* TCDTW_FLAG_* */
     float *phase_ms;        /* host, nullable: TCDTW_PHASES per-phase CUDA-event times */
+    /* Candidate-side index (ABI version 2): envelopes of
+     * this shard's candidates, (n_candidates, n, dims) of `dtype`, built with
+     * tcdtw_build_envelope at window min(window, n-1).  Read only with
+     * TCDTW_FLAG_REVERSE_LB, which prunes on max(LB_MV(c, env(q)),
+     * LB_MV(q, env(c))): DTW is symmetric in its arguments for equal lengths,
+     * so both are lower bounds (an extension; the reference's "switch the
+     * role" idea).  The in-DTW cascade keeps using the
+     * forward terms. */
+    const void *cand_upper;
+    const void *cand_lower;
 } tcdtw_search_desc;
 
-#define TCDTW_FLAG_TIMING 1 /* fill desc->phase_ms (synchronises the stream) */
+#define TCDTW_FLAG_TIMING 1     /* fill desc->phase_ms (synchronises the stream) */
+#define TCDTW_FLAG_REVERSE_LB 2 /* also prune on the candidate-envelope bound */
 #define TCDTW_PHASES 8      /* prep, lb_mv, seeds_topk, seeds_dtw, compact, advanced, dtw, finalize */
 #define TCDTW_COUNTERS 9    /* per query: see enum below */
 

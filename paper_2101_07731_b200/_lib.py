@@ -23,6 +23,7 @@ PHASES = ("prep", "lb_mv", "seeds_topk", "seeds_dtw", "compact", "advanced", "dt
 COUNTERS = ("dtw_computed", "dtw_skipped", "lb_mv_evals", "advanced_lb_evals", "abandon_count",
             "dtw_cells", "finalists", "survivors", "cells_issued")
 FLAG_TIMING = 1
+FLAG_REVERSE_LB = 2
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -42,7 +43,7 @@ class SearchDesc(ctypes.Structure):
         ("group_width", _i32), ("trigger_ti", ctypes.c_double), ("trigger_pc", ctypes.c_double),
         ("min_cell_frac", ctypes.c_double), ("n_queries", _i64), ("n_candidates", _i64),
         ("candidate_base", _i64), ("seeds", _i32), ("flags", _i32),
-        ("phase_ms", ctypes.POINTER(ctypes.c_float)),
+        ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("cand_upper", _vp), ("cand_lower", _vp),
     ]
 
 

@@ -58,7 +58,7 @@ const char* tcdtw_strerror(int status) {
     }
 }
 
-int tcdtw_abi_version(void) { return 1; }
+int tcdtw_abi_version(void) { return 2; }
 
 unsigned long long tcdtw_launch_count(void) { return g_launches.load(); }
 

@@ -100,6 +100,104 @@ __global__ void envelope_kernel(const T* __restrict__ S, int64_t n_series, int n
     }
 }
 
+// Streaming envelope (the HBM-bound form, also the candidate-side index
+// build): a block stages G whole series (G*n*d contiguous elements) through
+// shared memory with 16-byte loads, then uses the van Herk / Gil-Werman
+// decomposition -- the series is cut into blocks of k = min(2W+1, n) points;
+// within each block a forward (prefix) and backward (suffix) running max/min
+// is kept -- so a clipped window [max(0,i-W), min(n-1,i+W)] is
+// max(suffix[lo], prefix[hi]) when it spans two blocks, prefix[hi] when it
+// starts a block, suffix[lo] otherwise (the last, partial block).  About six
+// comparisons per element instead of 2(2W+1); max/min are exact, and ties
+// keep the earliest index like envelope_kernel, so the result is
+// bit-identical to it (lb_mv.py:44-71).  Traffic: read n*d, write 2*n*d
+// elements per series.
+template <typename T>
+__global__ void __launch_bounds__(256) envelope_stream_kernel(const T* __restrict__ S, int64_t n_series, int n,
+                                                              int d, int w, int G, T* __restrict__ U,
+                                                              T* __restrict__ L) {
+    extern __shared__ __align__(16) unsigned char env_smem[];
+    const int nd = n * d;
+    const int cap = G * nd;
+    T* X = reinterpret_cast<T*>(env_smem);  // staged series
+    T* PX = X + cap;                         // prefix max / min, suffix max / min
+    T* PN = PX + cap;
+    T* SX = PN + cap;
+    T* SN = SX + cap;
+    const int k = 2 * w + 1 < n ? 2 * w + 1 : n;
+    const int nb = (n + k - 1) / k;
+    constexpr int V = 16 / sizeof(T);
+    using VT = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    const bool vec = (nd % V) == 0 && (reinterpret_cast<uintptr_t>(S) % 16) == 0 &&
+                     (reinterpret_cast<uintptr_t>(U) % 16) == 0 && (reinterpret_cast<uintptr_t>(L) % 16) == 0;
+    for (int64_t s0 = (int64_t)blockIdx.x * G; s0 < n_series; s0 += (int64_t)gridDim.x * G) {
+        const int g_here = (int)((n_series - s0) < G ? (n_series - s0) : G);
+        const int elems = g_here * nd;
+        const T* src = S + s0 * nd;
+        __syncthreads();  // previous group's readers are done with the buffers
+        if (vec) {
+            const VT* s4 = reinterpret_cast<const VT*>(src);
+            VT* x4 = reinterpret_cast<VT*>(X);
+            for (int e = threadIdx.x; e < elems / V; e += blockDim.x) x4[e] = __ldcs(s4 + e);
+        } else {
+            for (int e = threadIdx.x; e < elems; e += blockDim.x) X[e] = __ldcs(src + e);
+        }
+        __syncthreads();
+        // one thread per (series, dim, block): prefix and suffix runs
+        const int seqs = g_here * d * nb;
+        for (int q = threadIdx.x; q < seqs; q += blockDim.x) {
+            const int p = q % d, b = (q / d) % nb, g = q / (d * nb);
+            const int i0 = b * k, i1 = (i0 + k < n ? i0 + k : n) - 1;
+            const int base = g * nd + p;
+            T mx = X[base + i0 * d], mn = mx;
+            PX[base + i0 * d] = mx;
+            PN[base + i0 * d] = mn;
+            for (int i = i0 + 1; i <= i1; ++i) {
+                const T v = X[base + i * d];
+                mx = v > mx ? v : mx;  // earliest index wins ties
+                mn = v < mn ? v : mn;
+                PX[base + i * d] = mx;
+                PN[base + i * d] = mn;
+            }
+            mx = X[base + i1 * d];
+            mn = mx;
+            SX[base + i1 * d] = mx;
+            SN[base + i1 * d] = mn;
+            for (int i = i1 - 1; i >= i0; --i) {
+                const T v = X[base + i * d];
+                mx = v >= mx ? v : mx;  // walking backwards: the earlier index wins ties
+                mn = v <= mn ? v : mn;
+                SX[base + i * d] = mx;
+                SN[base + i * d] = mn;
+            }
+        }
+        __syncthreads();
+        // combine and stream out: consecutive threads -> consecutive elements
+        T* du = U + s0 * nd;
+        T* dl = L + s0 * nd;
+        for (int e = threadIdx.x; e < elems; e += blockDim.x) {
+            const int g = e / nd, r = e - g * nd, i = r / d, p = r - i * d;
+            const int lo = i - w < 0 ? 0 : i - w;
+            const int hi = i + w > n - 1 ? n - 1 : i + w;
+            const int a = g * nd + lo * d + p, c = g * nd + hi * d + p;
+            T ux, ln;
+            if (lo / k != hi / k) {
+                const T sx = SX[a], px = PX[c], sn = SN[a], pn = PN[c];
+                ux = px > sx ? px : sx;
+                ln = pn < sn ? pn : sn;
+            } else if (lo % k == 0) {
+                ux = PX[c];
+                ln = PN[c];
+            } else {
+                ux = SX[a];
+                ln = SN[a];
+            }
+            __stcs(du + e, ux);
+            __stcs(dl + e, ln);
+        }
+    }
+}
+
 // Sequential prefix sum with first-prefix abandoning (core.py:133-146).
 template <typename T>
 struct PrefixAbandon {
@@ -581,7 +679,35 @@ int pairs_lb_pc(int dtype, const void* c, const void* bl, const void* bh, int64_
 
 int series_envelope(int dtype, const void* s, int64_t ns, int n, int d, int w, void* u, void* l,
                     cudaStream_t st) {
+    if (ns <= 0) return TCDTW_OK;
     const int64_t total = ns * (int64_t)n * d;
+    const size_t es = dtype == TCDTW_F64 ? 8 : 4;
+    const size_t per_series = (size_t)5 * n * d * es;  // X, prefix max/min, suffix max/min
+    static const bool naive = getenv("TCDTW_ENV_NAIVE") != nullptr;  // A/B switch
+    if (!naive && per_series <= 48 * 1024) {
+        // ~30-48 KB of staging per block, several blocks per SM so that loads
+        // of one block overlap the compute of the others
+        int G = (int)((36 * 1024) / per_series);
+        G = G < 1 ? 1 : G;
+        const size_t smem = per_series * G;
+        int dev = 0, sms = 148, occ = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        auto go = [&](auto kern, auto* S, auto* U, auto* L) -> int {
+            if (smem > 48 * 1024 &&
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return TCDTW_CUDA_ERROR;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+            int64_t groups = (ns + G - 1) / G;
+            int64_t grid = (int64_t)(occ < 1 ? 1 : occ) * sms * 4;
+            if (grid > groups) grid = groups;
+            kern<<<(int)grid, 256, smem, st>>>(S, ns, n, d, w, G, U, L);
+            return launch_status();
+        };
+        if (dtype == TCDTW_F64)
+            return go(envelope_stream_kernel<double>, (const double*)s, (double*)u, (double*)l);
+        return go(envelope_stream_kernel<float>, (const float*)s, (float*)u, (float*)l);
+    }
     const int grid = grid_for(total, 256) > 148 * 64 ? 148 * 64 : grid_for(total, 256);
     if (dtype == TCDTW_F64)
         envelope_kernel<double><<<grid, 256, 0, st>>>((const double*)s, ns, n, d, w, (double*)u, (double*)l);

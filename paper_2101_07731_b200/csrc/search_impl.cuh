@@ -142,7 +142,7 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
                                                         const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                         int64_t Q, int64_t N, int n, int d, int TC,
                                                         T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
-                                                        int64_t c0, bool v16);
+                                                        int64_t c0, bool v16, bool trans);
 
 // asynchronous global -> shared copies; src_bytes < bytes zero-fills the rest
 __device__ __forceinline__ void cp_async_ca(void* dst, const void* src, int bytes, int src_bytes) {
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ 
                                                           const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                           int64_t Q, int64_t N, int n, int d, int TC,
                                                           T* __restrict__ out, T* __restrict__ ub_out, int ub_stride,
-                                                          bool v16) {
+                                                          bool v16, bool trans) {
     using Tile = MvTile<T, DMAX, EXACT>;
     constexpr int QT = Tile::QT, CTL = Tile::CT;
     // query tiles vary fastest: concurrently resident blocks share one
@@ -181,11 +181,12 @@ __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ 
     if constexpr (UB) {
         if (((int64_t)blockIdx.x / nqt) % ub_stride != 0) {
             lbmv_matrix_kernel_body<T, DMAX, EXACT, false, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0,
-                                                               v16);
+                                                               v16, trans);
             return;
         }
     }
-    lbmv_matrix_kernel_body<T, DMAX, EXACT, UB, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0, v16);
+    lbmv_matrix_kernel_body<T, DMAX, EXACT, UB, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0, v16,
+                                                    trans);
 }
 
 template <typename T, int DMAX, bool EXACT, bool UB, int DX>
@@ -193,7 +194,7 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
                                                         const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                         int64_t Q, int64_t N, int n, int d, int TC,
                                                         T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
-                                                        int64_t c0, bool v16) {
+                                                        int64_t c0, bool v16, bool trans) {
     using Tile = MvTile<T, DMAX, EXACT>;
     constexpr int M = Tile::M, QT = Tile::QT, CTL = Tile::CT;
     constexpr int VN = 16 / (int)sizeof(T);  // elements per 16-byte copy
@@ -373,7 +374,9 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
         for (int j = 0; j < M; ++j) {
             const int64_t c = c0 + tc * M + j;
             if (c < N) {
-                out[q * N + c] = total[i][j];
+                // trans: the reverse bound (envelope side = candidates) lands
+                // in the (query, candidate) layout of the forward matrix
+                out[trans ? c * Q + q : q * N + c] = total[i][j];
                 if constexpr (UB) ub_out[q * N + c] = ubt[i][j];
             }
         }
@@ -382,7 +385,7 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
 
 template <typename T, int DMAX, bool EXACT>
 int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int64_t Q, int64_t N, int n, int d,
-                       T* out, T* ub_out, cudaStream_t st, int ub_stride = 1) {
+                       T* out, T* ub_out, cudaStream_t st, int ub_stride = 1, bool trans = false) {
     using Tile = MvTile<T, DMAX, EXACT>;
     const bool ub = ub_out != nullptr;
     // two staging buffers of TC time steps each (layout us | ls | cs | qs)
@@ -412,7 +415,7 @@ int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int6
     const int64_t nct = (N + Tile::CT - 1) / Tile::CT;
     if (nqt * nct > 2147483647LL) return TCDTW_NOT_SUPPORTED;
     const unsigned grid = (unsigned)(nqt * nct);
-    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out, ub_stride, v16);
+    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out, ub_stride, v16, trans);
     return launch_status();
 }
 
@@ -505,10 +508,11 @@ static __global__ void seed_tiles_kernel(int64_t Q, int S, const int32_t* __rest
 
 // ------------------------------------------------------------- compaction
 template <typename T>
-__device__ __forceinline__ bool keep_pred(const T* __restrict__ lbrow, int64_t c, T thr, bool all,
-                                          const uint32_t* seeds_s, int ns) {
+__device__ __forceinline__ bool keep_pred(const T* __restrict__ lbrow, const T* __restrict__ lb2row, int64_t c,
+                                          T thr, bool all, const uint32_t* seeds_s, int ns) {
     if (!all) {
         if (!(lbrow[c] <= thr)) return false;
+        if (lb2row && !(lb2row[c] <= thr)) return false;  // reverse bound (TCDTW_FLAG_REVERSE_LB)
     }
     for (int k = 0; k < ns; ++k)
         if (seeds_s[k] == (uint32_t)c) return false;
@@ -516,7 +520,8 @@ __device__ __forceinline__ bool keep_pred(const T* __restrict__ lbrow, int64_t c
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) compact_count_kernel(const T* __restrict__ lb, int64_t N, int n_chunks,
+__global__ void __launch_bounds__(256) compact_count_kernel(const T* __restrict__ lb, const T* __restrict__ lb2,
+                                                            int64_t N, int n_chunks,
                                                             const T* __restrict__ dbest, Margins mg, bool all,
                                                             const uint32_t* __restrict__ seeds, const int32_t* __restrict__ seed_cnt,
                                                             int S, int64_t* __restrict__ chunk_cnt) {
@@ -529,10 +534,11 @@ __global__ void __launch_bounds__(256) compact_count_kernel(const T* __restrict_
     __syncthreads();
     const T thr = all ? T(0) : scale_up<T>(dbest[q], mg.prune);
     const T* row = lb ? lb + q * N : nullptr;
+    const T* row2 = lb2 ? lb2 + q * N : nullptr;
     const int64_t c0 = (int64_t)chunk * kChunk;
     const int64_t c1 = c0 + kChunk < N ? c0 + kChunk : N;
     int cnt = 0;
-    for (int64_t c = c0 + threadIdx.x; c < c1; c += 256) cnt += keep_pred<T>(row, c, thr, all, sd, ns) ? 1 : 0;
+    for (int64_t c = c0 + threadIdx.x; c < c1; c += 256) cnt += keep_pred<T>(row, row2, c, thr, all, sd, ns) ? 1 : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
@@ -545,7 +551,8 @@ __global__ void __launch_bounds__(256) compact_count_kernel(const T* __restrict_
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) compact_write_kernel(const T* __restrict__ lb, int64_t N, int n_chunks,
+__global__ void __launch_bounds__(256) compact_write_kernel(const T* __restrict__ lb, const T* __restrict__ lb2,
+                                                            int64_t N, int n_chunks,
                                                             const T* __restrict__ dbest, Margins mg, bool all,
                                                             const uint32_t* __restrict__ seeds, const int32_t* __restrict__ seed_cnt,
                                                             int S, const int64_t* __restrict__ chunk_off,
@@ -561,13 +568,14 @@ __global__ void __launch_bounds__(256) compact_write_kernel(const T* __restrict_
     __syncthreads();
     const T thr = all ? T(0) : scale_up<T>(dbest[q], mg.prune);
     const T* row = lb ? lb + q * N : nullptr;
+    const T* row2 = lb2 ? lb2 + q * N : nullptr;
     const int64_t c0 = (int64_t)chunk * kChunk;
     const int64_t c1 = c0 + kChunk < N ? c0 + kChunk : N;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int64_t base = base_s;
     for (int64_t cb = c0; cb < c1; cb += 256) {
         const int64_t c = cb + threadIdx.x;
-        const bool k = c < c1 && keep_pred<T>(row, c, thr, all, sd, ns);
+        const bool k = c < c1 && keep_pred<T>(row, row2, c, thr, all, sd, ns);
         const unsigned bal = __ballot_sync(0xffffffffu, k);
         if (lane == 0) wsum[wid] = __popc(bal);
         __syncthreads();
@@ -2678,7 +2686,7 @@ struct Plan {
     int64_t Q, N;
     int n, d, w, B, G, K, S, n_chunks;
     size_t es;  // element size
-    bool has_lb, exact;
+    bool has_lb, exact, rev;
     int64_t max_tiles;
     // byte offsets
     size_t o_qT, o_ub, o_done, o_fin;
@@ -2686,7 +2694,7 @@ struct Plan {
     int ub_ct, ub_stride;
     size_t o_up, o_lo, o_upT, o_loT, o_candT, o_steps, o_blo, o_bhi, o_bcnt, o_lb, o_seed, o_seedres,
         o_seedcnt, o_dbest, o_ccnt, o_coff, o_surv, o_res, o_tcnt, o_toff, o_tq, o_tb, o_tl, o_sq, o_sb, o_sl,
-        o_ctr, o_minv, o_min64, o_bidx, o_tctr, o_cub, o_fsc, o_tisc, o_qpad, total;
+        o_ctr, o_minv, o_min64, o_bidx, o_tctr, o_cub, o_fsc, o_tisc, o_qpad, o_cupT, o_cloT, o_lb2, total;
     int qpad_rows;
     size_t cub_bytes;
     int fin_threads, adv_warps;
@@ -2720,6 +2728,8 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     p.exact = dsc->dtype == TCDTW_F64;
     p.es = p.exact ? 8 : 4;
     p.has_lb = dsc->method != TCDTW_METHOD_NONE;
+    p.rev = p.has_lb && (dsc->flags & TCDTW_FLAG_REVERSE_LB) != 0;
+    if (p.rev && (!dsc->cand_upper || !dsc->cand_lower)) return TCDTW_INVALID_INPUT;
     p.S = p.has_lb ? (dsc->seeds > 0 ? dsc->seeds : 8) : 0;
     if (p.S > kSeedMax) return TCDTW_INVALID_INPUT;
     if (p.S > p.N) p.S = (int)p.N;
@@ -2748,6 +2758,9 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     p.o_bcnt = take((size_t)Q * p.G * 4);
     p.o_lb = take(p.has_lb ? (size_t)Q * N * es : 0);
     p.o_ub = take(p.has_lb ? (size_t)Q * N * es : 0);
+    p.o_cupT = take(p.rev ? (size_t)N * p.n * p.d * es : 0);
+    p.o_cloT = take(p.rev ? (size_t)N * p.n * p.d * es : 0);
+    p.o_lb2 = take(p.rev ? (size_t)Q * N * es : 0);
     p.o_seed = take((size_t)Q * kSeedMax * 4);
     p.o_seedres = take((size_t)Q * kSeedMax * es);
     p.o_seedcnt = take((size_t)Q * 4);
@@ -3017,6 +3030,15 @@ struct SearchImpl {
             TRY((launch_lbmv_matrix<T, DMAX, EXACT>(at<T>(ws, p.o_upT), at<T>(ws, p.o_loT), at<T>(ws, p.o_qT),
                                                     at<T>(ws, p.o_candT), p.Q, p.N, p.n, p.d, at<T>(ws, p.o_lb),
                                                     at<T>(ws, p.o_ub), st, p.ub_stride)));
+        if (p.rev) {
+            // reverse LB_MV: the candidates' envelopes against the queries,
+            // written transposed into the (query, candidate) layout
+            TRY(planarize<T>((const T*)dsc->cand_upper, p.N, p.n * p.d, at<T>(ws, p.o_cupT), st));
+            TRY(planarize<T>((const T*)dsc->cand_lower, p.N, p.n * p.d, at<T>(ws, p.o_cloT), st));
+            TRY((launch_lbmv_matrix<T, DMAX, EXACT>(at<T>(ws, p.o_cupT), at<T>(ws, p.o_cloT), nullptr,
+                                                    at<T>(ws, p.o_qT), p.N, p.Q, p.n, p.d, at<T>(ws, p.o_lb2),
+                                                    nullptr, st, 1, true)));
+        }
         dbg_stage(st, "lb_mv");
         tm.mark(2);
         if (p.S > 0) {
@@ -3067,7 +3089,8 @@ struct SearchImpl {
         int64_t* coff = at<int64_t>(ws, p.o_coff);
         dim3 cgrid((unsigned)p.n_chunks, (unsigned)p.Q);
         if (p.Q > 65535) return TCDTW_INVALID_INPUT;
-        compact_count_kernel<T><<<cgrid, 256, 0, st>>>(a.lb, p.N, p.n_chunks, a.dbest, a.mg, all,
+        const T* lb2 = p.rev ? at<T>(ws, p.o_lb2) : nullptr;
+        compact_count_kernel<T><<<cgrid, 256, 0, st>>>(a.lb, lb2, p.N, p.n_chunks, a.dbest, a.mg, all,
                                                        at<uint32_t>(ws, p.o_seed), at<int32_t>(ws, p.o_seedcnt), p.S,
                                                        ccnt);
         TRY(launch_status());
@@ -3078,7 +3101,7 @@ struct SearchImpl {
             return TCDTW_CUDA_ERROR;
         uint32_t* surv = at<uint32_t>(ws, p.o_surv);
         T* res = at<T>(ws, p.o_res);
-        compact_write_kernel<T><<<cgrid, 256, 0, st>>>(a.lb, p.N, p.n_chunks, a.dbest, a.mg, all,
+        compact_write_kernel<T><<<cgrid, 256, 0, st>>>(a.lb, lb2, p.N, p.n_chunks, a.dbest, a.mg, all,
                                                        at<uint32_t>(ws, p.o_seed), at<int32_t>(ws, p.o_seedcnt), p.S,
                                                        coff, surv, res);
         TRY(launch_status());
@@ -3116,17 +3139,29 @@ struct SearchImpl {
         }
         dbg_stage(st, "advanced");
         if constexpr (!EXACT) {
-            // the R-row lane kernel keeps one query per warp: hand it whole segments
+            // the R-row lane kernel keeps one query per warp: hand it whole
+            // segments, or, when segments are too few to occupy every warp
+            // (small collections: C1 has 3 chunks per query), pieces of about
+            // survivors / (4 x resident warps), at least 4 pairs per lane
             if (n_tiles > 0 && laner_rows(a, p.d, p.B) > 0) {
+                const int64_t surv_est = n_tiles * (int64_t)kTile;
+                const int64_t warps = (int64_t)sms * 16;
+                int seg_len = (int)kChunk;
+                if (n_tiles * (int64_t)kTile / kChunk < 4 * warps) {
+                    int64_t want = surv_est / (4 * warps);
+                    seg_len = 128;
+                    while (seg_len < want && seg_len < (int)kChunk) seg_len <<= 1;
+                }
+                if (const char* sl = getenv("TCDTW_SEG_LEN")) seg_len = atoi(sl);
                 seg_tiles_count_kernel<<<grid_for(n_seg, 256), 256, 0, st>>>(p.Q, p.n_chunks, coff, tcnt, nullptr,
-                                                                             (int)kChunk);
+                                                                             seg_len);
                 TRY(launch_status());
                 cb = p.cub_bytes;
                 if (cub::DeviceScan::ExclusiveSum(at<void>(ws, p.o_cub), cb, tcnt, toff, (int)(n_seg + 1), st) !=
                     cudaSuccess)
                     return TCDTW_CUDA_ERROR;
                 seg_tiles_fill_kernel<<<grid_for(n_seg, 128), 128, 0, st>>>(p.Q, p.n_chunks, coff, toff, tl,
-                                                                            (int)kChunk);
+                                                                            seg_len);
                 TRY(launch_status());
                 cudaMemcpyAsync(&n_tiles, toff + n_seg, 8, cudaMemcpyDeviceToHost, st);
                 cudaStreamSynchronize(st);

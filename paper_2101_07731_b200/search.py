@@ -139,14 +139,41 @@ class SearchIndex:
         self.base = int(base)
         self._ws = None
         self._ws_bytes = 0
+        self._cenv = None  # (window, upper, lower): candidate-side index
 
     @property
     def n_candidates(self) -> int:
         return int(self.candidates.shape[0])
 
+    def candidate_envelopes(self, window: int):
+        """Candidate-side index: the LB_MV envelope of
+        every candidate at the effective window, built once per window by the
+        streaming envelope kernel and kept resident next to the collection.
+        It enables the reverse bound LB_MV(q, env(c)) (``reverse_bound=True``
+        in ``search``), the reference's "switch the role" idea."""
+        n = int(self.candidates.shape[1])
+        w = min(int(window), n - 1)
+        if w < 0:
+            raise InvalidInputError("window must be >= 0")
+        if self._cenv is None or self._cenv[0] != w:
+            self._cenv = None
+            up = _dev.empty(tuple(self.candidates.shape), self.tdtype)
+            lo = _dev.empty(tuple(self.candidates.shape), self.tdtype)
+            N, n, d = self.candidates.shape
+            _lib.check(_lib.lib().tcdtw_build_envelope(_lib.dtype_code(self.dtype), self.candidates.data_ptr(), N, n,
+                                                       d, w, up.data_ptr(), lo.data_ptr(), _lib.stream_ptr()),
+                       "build_envelope")
+            self._cenv = (w, up, lo)
+        return self._cenv[1], self._cenv[2]
+
     def _desc(self, params: SearchParams, adv: Method | None, n_q: int, seeds: int, timing: bool,
-              phase_buf) -> _lib.SearchDesc:
+              phase_buf, reverse_bound: bool = False) -> _lib.SearchDesc:
         _, n, d = self.candidates.shape
+        flags = _lib.FLAG_TIMING if timing else 0
+        cu = cl = None
+        if reverse_bound and params.method != Method.NONE:
+            cu, cl = self.candidate_envelopes(params.window)
+            flags |= _lib.FLAG_REVERSE_LB
         return _lib.SearchDesc(
             dtype=_lib.dtype_code(self.dtype), n=n, dims=d, window=int(params.window),
             method=METHOD_CODE[params.method],
@@ -155,12 +182,13 @@ class SearchIndex:
             max_boxes=params.max_boxes, group_width=params.group_width, trigger_ti=params.trigger_ti,
             trigger_pc=params.trigger_pc, min_cell_frac=params.min_cell_frac, n_queries=n_q,
             n_candidates=self.n_candidates, candidate_base=self.base, seeds=seeds,
-            flags=_lib.FLAG_TIMING if timing else 0,
-            phase_ms=ctypes.cast(phase_buf, ctypes.POINTER(ctypes.c_float)) if timing else None)
+            flags=flags, phase_ms=ctypes.cast(phase_buf, ctypes.POINTER(ctypes.c_float)) if timing else None,
+            cand_upper=_lib.ptr(cu), cand_lower=_lib.ptr(cl))
 
-    def workspace_bytes(self, params: SearchParams, advanced=None, n_q: int = 1, seeds: int = 0) -> int:
+    def workspace_bytes(self, params: SearchParams, advanced=None, n_q: int = 1, seeds: int = 0,
+                        reverse_bound: bool = False) -> int:
         adv = _advanced_method(params, advanced)
-        desc = self._desc(params, adv, n_q, seeds, False, None)
+        desc = self._desc(params, adv, n_q, seeds, False, None, reverse_bound)
         out = ctypes.c_size_t()
         _lib.check(_lib.load_library().tcdtw_search_workspace_size(ctypes.byref(desc), ctypes.byref(out)),
                    "workspace_size")
@@ -173,7 +201,7 @@ class SearchIndex:
         return _lib.load_library().tcdtw_dtw_kernel_name(ctypes.byref(desc)).decode()
 
     def auto_batch(self, params: SearchParams, advanced=None, n_q: int = 1, budget_bytes: int | None = None,
-                   seeds: int = 0) -> int:
+                   seeds: int = 0, reverse_bound: bool = False) -> int:
         """Largest query batch whose workspace fits the budget (default:
         half of the free device memory)."""
         t = _dev.torch()
@@ -181,11 +209,11 @@ class SearchIndex:
             free, _ = t.cuda.mem_get_info()
             budget_bytes = int(free * 0.5)
         lo, hi = 1, max(1, int(n_q))
-        if self.workspace_bytes(params, advanced, hi, seeds) <= budget_bytes:
+        if self.workspace_bytes(params, advanced, hi, seeds, reverse_bound) <= budget_bytes:
             return hi
         while lo < hi:
             mid = (lo + hi + 1) // 2
-            if self.workspace_bytes(params, advanced, mid, seeds) <= budget_bytes:
+            if self.workspace_bytes(params, advanced, mid, seeds, reverse_bound) <= budget_bytes:
                 lo = mid
             else:
                 hi = mid - 1
@@ -202,6 +230,7 @@ class SearchIndex:
     def release(self):
         self._ws = None
         self._ws_bytes = 0
+        self._cenv = None
 
     def prepare_queries(self, queries):
         t = _dev.torch()
@@ -217,14 +246,14 @@ class SearchIndex:
         return Q
 
     def seed_phase(self, qp, params: SearchParams, advanced=None, dim_range=None, seeds: int = 0,
-                   timing: bool = False) -> dict:
+                   timing: bool = False, reverse_bound: bool = False) -> dict:
         """Phase 1 (tcdtw_search_seed) for one query batch already on the
         device; returns the state whose ``dbest`` a sharded caller may
         min-reduce before ``finish_phase``."""
         t = _dev.torch()
         adv = _advanced_method(params, advanced)
         phase_buf = (ctypes.c_float * len(_lib.PHASES))()
-        desc = self._desc(params, adv, int(qp.shape[0]), seeds, timing, phase_buf)
+        desc = self._desc(params, adv, int(qp.shape[0]), seeds, timing, phase_buf, reverse_bound)
         nbytes = ctypes.c_size_t()
         L = _lib.lib()
         _lib.check(L.tcdtw_search_workspace_size(ctypes.byref(desc), ctypes.byref(nbytes)), "workspace_size")
@@ -259,17 +288,20 @@ class SearchIndex:
         return out_idx, out_dist, out_ctr
 
     def search(self, queries, params: SearchParams, advanced=None, dim_range=None, batch: int | None = None,
-               seeds: int = 0, timing: bool = False, dbest_hook=None, return_device: bool = False) -> BatchOutcome:
+               seeds: int = 0, timing: bool = False, dbest_hook=None, return_device: bool = False,
+               reverse_bound: bool = False) -> BatchOutcome:
         """1-NN of every query.  `dbest_hook(d_best_tensor)` (optional) may
         tighten the per-query best-so-far between the two phases, e.g. an
         NCCL min-allreduce across shards.  With return_device=True the
-        result arrays stay on the GPU (torch tensors)."""
+        result arrays stay on the GPU (torch tensors).  reverse_bound=True
+        also prunes on the candidate-envelope bound (candidate_envelopes);
+        the answers are the same, only the counters change."""
         t = _dev.torch()
         _advanced_method(params, advanced)
         Q = self.prepare_queries(queries)
         n_q = Q.shape[0]
         if batch is None:
-            batch = self.auto_batch(params, advanced, n_q, seeds=seeds)
+            batch = self.auto_batch(params, advanced, n_q, seeds=seeds, reverse_bound=reverse_bound)
         batch = max(1, min(int(batch), n_q))
         best_idx = t.empty(n_q, dtype=t.int64, device=Q.device)
         best_dist = t.empty(n_q, dtype=t.float64, device=Q.device)
@@ -278,7 +310,7 @@ class SearchIndex:
         t_start = time.perf_counter()
         for q0 in range(0, n_q, batch):
             q1 = min(n_q, q0 + batch)
-            st = self.seed_phase(Q[q0:q1], params, advanced, dim_range, seeds, timing)
+            st = self.seed_phase(Q[q0:q1], params, advanced, dim_range, seeds, timing, reverse_bound)
             if timing:
                 phase_tot[:4] += np.array(st["seed_ms"])
             if dbest_hook is not None:

@@ -62,6 +62,29 @@ def test_envelope_golden(P):
         assert env.window == case["weff"]
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_envelope_stream_shapes(P, rng, dtype):
+    """The staged van Herk envelope kernel (whole stacks, ragged last group,
+    odd n*d without 16-byte loads, W = 0, W >= n, blocks of one point) is
+    bit-identical to the oracle's sliding max/min (lb_mv.py:44-88)."""
+    from oracle import oracle as O
+    from paper_2101_07731_b200.lb_mv import build_envelopes
+
+    for S, n, d, w in ((37, 128, 6, 12), (11, 64, 20, 6), (9, 33, 3, 5), (5, 17, 1, 0), (7, 10, 4, 40),
+                       (6, 25, 5, 12), (13, 31, 7, 3), (3, 1, 2, 2)):
+        X = rng.normal(size=(S, n, d)).astype(dtype)
+        X[0, :, 0] = 0.0  # constant runs: ties everywhere
+        import torch
+
+        up, lo = build_envelopes(X, w, dtype=torch.float32 if dtype == np.float32 else None)
+        assert up.dtype == (torch.float32 if dtype == np.float32 else torch.float64)
+        up, lo = up.cpu().numpy(), lo.cpu().numpy()
+        for s in range(S):
+            ou, ol = O.build_envelope(X[s].astype(np.float64), min(w, n - 1))
+            assert np.array_equal(up[s].astype(np.float64), ou), (S, n, d, w, s)
+            assert np.array_equal(lo[s].astype(np.float64), ol), (S, n, d, w, s)
+
+
 def test_lb_mv_lb_ad_steps_golden(P):
     for case in load_cases("lb_mv_ad"):
         env = P.build_envelope(case["q"], case["w"])
