@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exchange", action="store_true", help="skip the d_best all-reduce between phases")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (testing)")
+    ap.add_argument("--reverse-bound", action="store_true",
+                    help="also prune on LB_MV(q, env(c)) from the candidate-side index (SURVEY 8f f2)")
     return ap.parse_args()
 
 
@@ -138,6 +140,46 @@ def measured_peaks():
         except Exception:
             pass
     return {}
+
+
+def index_envelope_stats(index, w, _lib, reps=5):
+    """The candidate-side index build: envelopes of the whole
+    shard by the streaming envelope kernel, timed with CUDA events on the
+    launching stream.  HBM-bound: reads n*d and writes 2*n*d elements per
+    series (3*N*L*d*s bytes)."""
+    import torch
+
+    N, n, d = index.candidates.shape
+    es = index.candidates.element_size()
+    up = torch.empty_like(index.candidates)
+    lo = torch.empty_like(index.candidates)
+    code = _lib.dtype_code(index.dtype)
+    L = _lib.lib()
+    weff = min(int(w), n - 1)
+
+    def go():
+        _lib.check(L.tcdtw_build_envelope(code, index.candidates.data_ptr(), N, n, d, weff, up.data_ptr(),
+                                          lo.data_ptr(), _lib.stream_ptr()), "build_envelope")
+
+    go()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        go()
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = statistics.median(ms)
+    nbytes = 3 * N * n * d * es
+    peak = measured_peaks().get("hbm_gbs")
+    gbs = nbytes / (t / 1e3) / 1e9
+    del up, lo
+    return {"kernel": "envelope_stream_kernel", "bound": "hbm", "series": int(N), "ms": t,
+            "algorithmic_bytes": nbytes, "achieved": gbs, "peak": peak, "unit": "GB/s",
+            "frac": gbs / peak if peak else None,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver copy test)"}
 
 
 # -------------------------------------------------------- CPU (oracle) legs
@@ -265,9 +307,10 @@ def run_ours(args):
     index = P.SearchIndex(wl.candidates[a:b], dtype=wl.dtype, base=a)
     torch.cuda.synchronize()
     t_up = time.perf_counter() - t_up
+    env_stats = index_envelope_stats(index, w, _lib)
     Qdev = index.prepare_queries(wl.queries)
     n_q = Qdev.shape[0]
-    batch = args.batch or index.auto_batch(params, advanced, n_q, seeds=args.seeds)
+    batch = args.batch or index.auto_batch(params, advanced, n_q, seeds=args.seeds, reverse_bound=args.reverse_bound)
     if world > 1:  # every rank must run the same batches (one d_best exchange per batch)
         bt = torch.tensor([batch], dtype=torch.int64, device="cuda")
         torch.distributed.all_reduce(bt, op=torch.distributed.ReduceOp.MIN)
@@ -279,7 +322,8 @@ def run_ours(args):
 
     def step(queries, to_host=False):
         res = index.search(queries, params, advanced=advanced, dim_range=wl.dim_range, batch=batch,
-                           seeds=args.seeds, dbest_hook=hook, return_device=True)
+                           seeds=args.seeds, dbest_hook=hook, return_device=True,
+                           reverse_bound=args.reverse_bound)
         idx, dist_ = res.best_index, res.best_distance
         if world > 1:
             idx, dist_ = combine_results(idx, dist_, group)
@@ -325,7 +369,7 @@ def run_ours(args):
 
     # instrumented pass: phase times (CUDA events per phase), counters
     res = index.search(Qdev, params, advanced=advanced, dim_range=wl.dim_range, batch=batch, seeds=args.seeds,
-                       timing=True, dbest_hook=hook, return_device=True)
+                       timing=True, dbest_hook=hook, return_device=True, reverse_bound=args.reverse_bound)
     ph = res.phase_ms
     ctr = {k: v.sum().item() for k, v in res.counters.items()}
     if world > 1:
@@ -394,6 +438,7 @@ def run_ours(args):
                        "advanced": None if advanced is None else advanced.value,
                        "trigger_ti": params.trigger_ti, "trigger_pc": params.trigger_pc,
                        "quant_levels": params.quant_levels, "query_batch": batch,
+                       "reverse_bound": bool(args.reverse_bound),
                        "parallelism": f"candidate shards x{world}",
                        "l2": "inputs larger than L2 (collection resident in HBM, no flush)"},
             "e2e": {"value": n_q / (e2e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": q_bytes,
@@ -403,6 +448,7 @@ def run_ours(args):
             "counters": {k: ctr[k] for k in _lib.COUNTERS},
             "phase_ms": ph,
             "roofline": roof,
+            "index_envelope": env_stats,
             "clocks": clocks,
             "cpu_baseline": cpu,
             "setup_s": {"generate": t_gen, "upload": t_up},

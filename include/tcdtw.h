@@ -214,6 +214,22 @@ int tcdtw_lb_mv_matrix(int dtype, const void *upper, const void *lower, const vo
  * (informational; a static string). */
 const char *tcdtw_dtw_kernel_name(const tcdtw_search_desc *desc);
 
+/* ---------------------------------------------------------------------- */
+/* Device-side ingest.                                   */
+/* ---------------------------------------------------------------------- */
+
+/* normalize(ds) -> Dataset(values, dim_ranges), ingest.py:245-261, on the
+ * device: values (n_points, dims) float64 with NaN marking missing entries
+ * (n_points = num_series * length); out (n_points, dims) z-normalised per
+ * dimension with the population mean/std over all points (missing values
+ * enter as raw zeros, zero-variance dimensions become all-zeros); mean, std,
+ * range (dims,) -- range is the post-normalisation max - min
+ * (ingest.py:235-237), the LB_PC dim_range.  Deterministic tree reductions:
+ * statistics equal the reference's to rounding.  out may alias values. */
+int tcdtw_normalize_workspace_size(int32_t dims, size_t *bytes);
+int tcdtw_normalize(const double *values, int64_t n_points, int32_t dims, double *out, double *mean,
+                    double *std, double *range, void *workspace, size_t ws_bytes, void *stream);
+
 /* Issue-rate probe: a dependent-chain-free FFMA/DFMA loop, for measuring
  * the ALU roofline on the box.  Returns lane-operations issued. */
 int tcdtw_alu_probe(int dtype, int32_t blocks, int32_t iters, void *sink, double *lane_ops,

@@ -63,6 +63,8 @@ _SIGS = {
                               _vp, _vp, _vp, _vp], ctypes.c_int),
     "tcdtw_lb_pc": ([ctypes.c_int, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
                     ctypes.c_int),
+    "tcdtw_normalize_workspace_size": ([_i32, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "tcdtw_normalize": ([_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp], ctypes.c_int),
     "tcdtw_search_workspace_size": ([ctypes.POINTER(SearchDesc), ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "tcdtw_search_seed": ([ctypes.POINTER(SearchDesc), _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp], ctypes.c_int),
     "tcdtw_search_finish": ([ctypes.POINTER(SearchDesc), _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp,

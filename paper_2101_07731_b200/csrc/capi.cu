@@ -34,6 +34,8 @@ int search_finish(const tcdtw_search_desc*, const void*, const void*, const void
 int lb_mv_matrix(int, const void*, const void*, const void*, int64_t, int64_t, int, int, void*, cudaStream_t);
 int alu_probe(int, int, int, void*, double*, cudaStream_t);
 const char* dtw_kernel_name(const tcdtw_search_desc*);
+size_t normalize_workspace_bytes(int);
+int normalize_f64(const double*, int64_t, int, double*, double*, double*, double*, double*, cudaStream_t);
 }  // namespace tcdtw
 
 using namespace tcdtw;
@@ -190,4 +192,18 @@ int tcdtw_alu_probe(int dtype, int32_t blocks, int32_t iters, void* sink, double
     return alu_probe(dtype, blocks, iters, sink, lane_ops, S(stream));
 }
 
+
+int tcdtw_normalize_workspace_size(int32_t dims, size_t* bytes) {
+    if (dims < 1 || dims > kMaxDims || !bytes) return TCDTW_INVALID_INPUT;
+    *bytes = normalize_workspace_bytes(dims);
+    return TCDTW_OK;
+}
+
+int tcdtw_normalize(const double* values, int64_t n_points, int32_t dims, double* out, double* mean, double* std_,
+                    double* range, void* workspace, size_t ws_bytes, void* stream) {
+    if (n_points < 1 || dims < 1 || dims > kMaxDims) return TCDTW_INVALID_INPUT;  // ingest.py:62-63
+    if (!values || !out || !mean || !std_ || !range) return TCDTW_INVALID_INPUT;
+    if (!workspace || ws_bytes < normalize_workspace_bytes(dims)) return TCDTW_WORKSPACE_TOO_SMALL;
+    return normalize_f64(values, n_points, dims, out, mean, std_, range, (double*)workspace, S(stream));
+}
 }  // extern "C"

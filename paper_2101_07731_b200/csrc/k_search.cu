@@ -74,6 +74,13 @@ const char* dtw_kernel_name(const tcdtw_search_desc* dsc) {
     }
     if (p.B <= 64) return "dtw_tpp_kernel";
     if (getenv("TCDTW_PIPE") && p.w >= 32) return "dtw_pipe_kernel";
+    if (!getenv("TCDTW_WAVE_GENERIC")) {
+        bool wd = false;
+#define TCDTW_WAVE_NAME(DD) wd = wd || p.d == DD;
+        TCDTW_WAVE_DIMS(TCDTW_WAVE_NAME)
+#undef TCDTW_WAVE_NAME
+        if (wd) return "dtw_wave_d_kernel";
+    }
     return "dtw_wave_kernel";
 }
 

@@ -1865,6 +1865,135 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
     }
 }
 
+// The same wavefront with the dimension count a compile-time constant and a
+// branch-free step: every lane evaluates its cell (inactive lanes on a
+// clamped query row, the result replaced by +inf), lane 0 takes the row above
+// from the handoff row by a predicated load, and the only synchronisation per
+// step is the shuffle.  The per-step cost drops from ~148 warp instructions
+// (runtime d: address arithmetic, guards, reconvergence) to the DP's own
+// arithmetic plus a few selects (C3: fp64, d = 8).  Row-granular abandoning
+// and the float64 arithmetic order are those of dtw_wave_kernel.
+template <typename T, int D, bool EXACT>
+__global__ void __launch_bounds__(256) dtw_wave_d_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
+                                                         const uint32_t* __restrict__ cand_of, T* __restrict__ res,
+                                                         int* __restrict__ tile_ctr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int SP = (D % 2 == 1) ? D : D + 1;  // odd word stride: conflict-free column reads
+    const int n = a.n, w = a.w, B = 2 * w + 1;
+    const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* qs = reinterpret_cast<T*>(smem_raw);                          // (n + 2w) * SP
+    T* prow = qs + (size_t)(n + 2 * w) * SP + (size_t)wib * (B + 1);  // per warp: B + 1 (last = +inf)
+    __shared__ int64_t tile_s;
+    const T INF = dev_inf<T>();
+    const unsigned FULL = 0xffffffffu;
+    const int qmax = n + 2 * w - 1;
+    int64_t cached_q = -1;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1);
+        __syncthreads();
+        const int64_t tile = tile_s;
+        if (tile >= n_tiles) break;
+        const int64_t q = tl.q[tile];
+        const int64_t e0 = tl.begin[tile];
+        const int len = tl.len[tile];
+        if (q != cached_q) {
+            const T* qsrc = a.queries + q * (int64_t)n * D;
+            for (int e = threadIdx.x; e < (n + 2 * w) * D; e += blockDim.x) {
+                const int r = e / D, p = e - (e / D) * D;
+                const int j = r - w;
+                qs[r * SP + p] = (j >= 0 && j < n) ? qsrc[(int64_t)j * D + p] : INF;
+            }
+            cached_q = q;
+            __syncthreads();
+        }
+        for (int slot = wib; slot < len; slot += warps) {
+            const int64_t ent = e0 + slot;
+            if (res[ent] < T(0)) continue;  // pruned by the advanced bound (warp-uniform)
+            const int64_t c = cand_of[ent];
+            const T* crow = a.cands + c * (int64_t)n * D;
+            for (int k = lane; k <= B; k += 32) prow[k] = (k == w) ? T(0) : INF;
+            __syncwarp();
+            T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg.prune) : INF;
+            bool abandoned = false;
+            int stop_row = n - 1;
+            for (int i0 = 0; i0 < n; i0 += 32) {
+                const int i = i0 + lane;
+                const bool valid = i < n;
+                const bool writer = valid && (lane == 31 || i == n - 1);
+                T rp[D];
+                {
+                    const T* src = crow + (int64_t)(valid ? i : n - 1) * D;
+#pragma unroll
+                    for (int p = 0; p < D; ++p) rp[p] = src[p];
+                }
+                const int rows_here = n - i0 < 32 ? n - i0 : 32;
+                const int steps = B + 2 * (rows_here - 1);
+                T mine = INF, got = INF, rmin = INF;
+                for (int tau = 0; tau < steps; ++tau) {
+                    const int k = tau - 2 * lane;
+                    const T got_prev = got;
+                    got = __shfl_up_sync(FULL, mine, 1);
+                    const bool act = valid && (unsigned)k < (unsigned)B;
+                    const int kc = k < 0 ? 0 : (k > B - 1 ? B - 1 : k);
+                    T up = got, dg = got_prev;
+                    if (lane == 0) {
+                        up = prow[kc + 1];  // prow[B] = +inf
+                        dg = prow[kc];
+                    }
+                    int qr = i + k;
+                    qr = qr < 0 ? 0 : (qr > qmax ? qmax : qr);
+                    const T* qp = qs + qr * SP;
+                    T cost;
+                    if constexpr (EXACT) {
+                        cost = dist_exact<T, D>(rp, qp, D);
+                    } else {
+                        T s = T(0);
+#pragma unroll
+                        for (int p = 0; p < D; ++p) {
+                            const T df = rp[p] - qp[p];
+                            s = fma(df, df, s);
+                        }
+                        cost = fast_sqrt(s);
+                    }
+                    const T best = tmin(tmin(up, dg), mine);
+                    T v = EXACT ? add_rn(cost, best) : cost + best;
+                    v = act ? v : INF;
+                    rmin = tmin(rmin, v);
+                    mine = v;
+                    if (act && writer) prow[k] = v;
+                }
+                __syncwarp();  // the handoff row is complete for the next chunk
+                const unsigned bad = __ballot_sync(FULL, valid && rmin > thr);
+                if (bad) {
+                    abandoned = true;
+                    stop_row = i0 + __ffs(bad) - 1;
+                    break;
+                }
+                if (a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg.prune);
+            }
+            const T fin = abandoned ? INF : prow[w];  // row n-1, column n-1
+            if (!abandoned && fin > thr) abandoned = true;  // dtw.py:101-102
+            if (lane == 0) {
+                res[ent] = abandoned ? INF : fin;
+                if (!abandoned) {
+                    atomic_min_nonneg<T>(a.dbest + q, fin);
+                    note_done(a, q, ent);
+                }
+                int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
+                atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_DTW_COMPUTED), 1ull);
+                if (abandoned) atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_ABANDON_COUNT), 1ull);
+                atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_DTW_CELLS),
+                          (unsigned long long)cells_upto(stop_row, n, w));
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// dimension counts with a compile-time wavefront kernel
+#define TCDTW_WAVE_DIMS(X) X(3) X(4) X(5) X(6) X(8)
+
 // ------------------- DTW, warp per pair, continuous row pipeline (W >= 32)
 // Lane l owns rows l, l+32, l+64, ...; row r = l + 32m sweeps its 2W+1 band
 // columns in consecutive steps starting at S(r) = m(2W+1) + 2l, so lanes stay
@@ -2976,6 +3105,29 @@ static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tile
         if (grid > n_tiles) grid = n_tiles;
         kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
         return launch_status();
+    }
+    const size_t smem_d = ((size_t)(p.n + 2 * p.w) * ((p.d % 2 == 1) ? p.d : p.d + 1) + (size_t)8 * (p.B + 1)) *
+                          sizeof(T);
+    auto run_d = [&](auto kern) -> int {
+        if (smem_d > 48 * 1024 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d) != cudaSuccess)
+            return TCDTW_NOT_SUPPORTED;
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem_d);
+        if (occ < 1) return TCDTW_NOT_SUPPORTED;
+        int64_t grid = (int64_t)occ * sms;
+        if (grid > n_tiles) grid = n_tiles;
+        kern<<<(int)grid, 256, smem_d, st>>>(a, tl, n_tiles, cand_of, res, tctr);
+        return launch_status();
+    };
+    if (!getenv("TCDTW_WAVE_GENERIC")) {  // A/B switch
+#define TCDTW_WAVE_CASE(DD)                                            \
+        if (p.d == DD && DD <= DMAX) {                                 \
+            const int s = run_d(dtw_wave_d_kernel<T, (DD <= DMAX ? DD : 1), EXACT>); \
+            if (s != TCDTW_NOT_SUPPORTED) return s;                    \
+        }
+        TCDTW_WAVE_DIMS(TCDTW_WAVE_CASE)
+#undef TCDTW_WAVE_CASE
     }
     const size_t smem = ((size_t)(p.n + 2 * p.w) * ((p.d % 2 == 1) ? p.d : p.d + 1) + (size_t)8 * p.B) * sizeof(T);
     auto kern = dtw_wave_kernel<T, DMAX, EXACT>;
