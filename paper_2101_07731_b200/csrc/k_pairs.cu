@@ -101,101 +101,149 @@ __global__ void envelope_kernel(const T* __restrict__ S, int64_t n_series, int n
 }
 
 // Streaming envelope (the HBM-bound form, also the candidate-side index
-// build): a block stages G whole series (G*n*d contiguous elements) through
-// shared memory with 16-byte loads, then uses the van Herk / Gil-Werman
-// decomposition -- the series is cut into blocks of k = min(2W+1, n) points;
-// within each block a forward (prefix) and backward (suffix) running max/min
-// is kept -- so a clipped window [max(0,i-W), min(n-1,i+W)] is
-// max(suffix[lo], prefix[hi]) when it spans two blocks, prefix[hi] when it
-// starts a block, suffix[lo] otherwise (the last, partial block).  About six
-// comparisons per element instead of 2(2W+1); max/min are exact, and ties
-// keep the earliest index like envelope_kernel, so the result is
-// bit-identical to it (lb_mv.py:44-71).  Traffic: read n*d, write 2*n*d
-// elements per series.
+// build).  A persistent block walks groups of G whole series (G*n*d
+// contiguous elements):
+//   * the next group streams into a second staging buffer by 16-byte
+//     cp.async while the current one is processed, so HBM reads are always in
+//     flight (without it the kernel sat at ~27% of the copy bandwidth);
+//   * van Herk / Gil-Werman: the series is cut into blocks of k = min(2W+1, n)
+//     points, and four independent scans per (series, dim, block) -- prefix
+//     max, prefix min, suffix max, suffix min -- run on four threads, so a
+//     clipped window [max(0,i-W), min(n-1,i+W)] is max(suffix[lo],
+//     prefix[hi]) when it spans two blocks, prefix[hi] when it starts a block
+//     and suffix[lo] otherwise (the last, partial block): about six
+//     comparisons per element instead of 2(2W+1);
+//   * the combine walks each series row by row with the dimension count a
+//     compile-time constant (no integer division per element) and streams
+//     the results out (read n*d, write 2*n*d elements per series).
+// max/min are exact and ties keep the earliest index, like envelope_kernel,
+// so the result is bit-identical to it (lb_mv.py:44-71).
 template <typename T>
+__device__ __forceinline__ void env_cp16(T* dst, const T* src) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
+}
+
+template <typename T, int DC>  // DC > 0: compile-time dimension count
 __global__ void __launch_bounds__(256) envelope_stream_kernel(const T* __restrict__ S, int64_t n_series, int n,
-                                                              int d, int w, int G, T* __restrict__ U,
+                                                              int d_rt, int w, int G, T* __restrict__ U,
                                                               T* __restrict__ L) {
     extern __shared__ __align__(16) unsigned char env_smem[];
+    const int d = DC > 0 ? DC : d_rt;
     const int nd = n * d;
     const int cap = G * nd;
-    T* X = reinterpret_cast<T*>(env_smem);  // staged series
-    T* PX = X + cap;                         // prefix max / min, suffix max / min
+    T* X0 = reinterpret_cast<T*>(env_smem);  // two staging buffers
+    T* X1 = X0 + cap;
+    T* PX = X1 + cap;                        // prefix max / min, suffix max / min
     T* PN = PX + cap;
     T* SX = PN + cap;
     T* SN = SX + cap;
+    int2* tab = reinterpret_cast<int2*>(SN + cap);  // per row: the two max operands' offsets from PX
     const int k = 2 * w + 1 < n ? 2 * w + 1 : n;
     const int nb = (n + k - 1) / k;
+    // per-row window table, once per launch (the divisions by the runtime
+    // block length stay out of the per-element work).  The window max is
+    // max(A, B) with A, B offsets from PX: SX[lo] and PX[hi] when the window
+    // spans two blocks, PX[hi] twice when it starts a block, SX[lo] twice
+    // otherwise; the min operands sit one array (cap) further (PN, SN).
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int lo = i - w < 0 ? 0 : i - w;
+        const int hi = i + w > n - 1 ? n - 1 : i + w;
+        const int sx = 2 * cap + lo * d, px = hi * d;
+        if (lo / k != hi / k) tab[i] = make_int2(sx, px);
+        else if (lo % k == 0) tab[i] = make_int2(px, px);
+        else tab[i] = make_int2(sx, sx);
+    }
     constexpr int V = 16 / sizeof(T);
-    using VT = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
-    const bool vec = (nd % V) == 0 && (reinterpret_cast<uintptr_t>(S) % 16) == 0 &&
-                     (reinterpret_cast<uintptr_t>(U) % 16) == 0 && (reinterpret_cast<uintptr_t>(L) % 16) == 0;
-    for (int64_t s0 = (int64_t)blockIdx.x * G; s0 < n_series; s0 += (int64_t)gridDim.x * G) {
+    const bool vec = (nd % V) == 0 && (reinterpret_cast<uintptr_t>(S) % 16) == 0;
+    const int64_t stride = (int64_t)gridDim.x * G;
+    auto stage = [&](int64_t s0, T* X) {  // issue the loads of group s0 (no wait)
+        if (s0 >= n_series) return;
         const int g_here = (int)((n_series - s0) < G ? (n_series - s0) : G);
         const int elems = g_here * nd;
         const T* src = S + s0 * nd;
-        __syncthreads();  // previous group's readers are done with the buffers
         if (vec) {
-            const VT* s4 = reinterpret_cast<const VT*>(src);
-            VT* x4 = reinterpret_cast<VT*>(X);
-            for (int e = threadIdx.x; e < elems / V; e += blockDim.x) x4[e] = __ldcs(s4 + e);
+            for (int e = threadIdx.x * V; e < elems; e += blockDim.x * V) env_cp16(X + e, src + e);
         } else {
-            for (int e = threadIdx.x; e < elems; e += blockDim.x) X[e] = __ldcs(src + e);
+            for (int e = threadIdx.x; e < elems; e += blockDim.x) X[e] = src[e];
         }
+    };
+    int64_t s0 = (int64_t)blockIdx.x * G;
+    stage(s0, X0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    T* X = X0;
+    T* Xn = X1;
+    for (; s0 < n_series; s0 += stride) {
+        stage(s0 + stride, Xn);  // Xn was released by the barrier after the last combine
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
-        // one thread per (series, dim, block): prefix and suffix runs
-        const int seqs = g_here * d * nb;
-        for (int q = threadIdx.x; q < seqs; q += blockDim.x) {
-            const int p = q % d, b = (q / d) % nb, g = q / (d * nb);
-            const int i0 = b * k, i1 = (i0 + k < n ? i0 + k : n) - 1;
-            const int base = g * nd + p;
-            T mx = X[base + i0 * d], mn = mx;
-            PX[base + i0 * d] = mx;
-            PN[base + i0 * d] = mn;
-            for (int i = i0 + 1; i <= i1; ++i) {
-                const T v = X[base + i * d];
-                mx = v > mx ? v : mx;  // earliest index wins ties
-                mn = v < mn ? v : mn;
-                PX[base + i * d] = mx;
-                PN[base + i * d] = mn;
-            }
-            mx = X[base + i1 * d];
-            mn = mx;
-            SX[base + i1 * d] = mx;
-            SN[base + i1 * d] = mn;
-            for (int i = i1 - 1; i >= i0; --i) {
-                const T v = X[base + i * d];
-                mx = v >= mx ? v : mx;  // walking backwards: the earlier index wins ties
-                mn = v <= mn ? v : mn;
-                SX[base + i * d] = mx;
-                SN[base + i * d] = mn;
-            }
-        }
-        __syncthreads();
-        // combine and stream out: consecutive threads -> consecutive elements
-        T* du = U + s0 * nd;
-        T* dl = L + s0 * nd;
-        for (int e = threadIdx.x; e < elems; e += blockDim.x) {
-            const int g = e / nd, r = e - g * nd, i = r / d, p = r - i * d;
-            const int lo = i - w < 0 ? 0 : i - w;
-            const int hi = i + w > n - 1 ? n - 1 : i + w;
-            const int a = g * nd + lo * d + p, c = g * nd + hi * d + p;
-            T ux, ln;
-            if (lo / k != hi / k) {
-                const T sx = SX[a], px = PX[c], sn = SN[a], pn = PN[c];
-                ux = px > sx ? px : sx;
-                ln = pn < sn ? pn : sn;
-            } else if (lo % k == 0) {
-                ux = PX[c];
-                ln = PN[c];
+        const int g_here = (int)((n_series - s0) < G ? (n_series - s0) : G);
+        // scans: one thread per (direction, series, block, dim); the forward
+        // thread keeps prefix max and min, the backward one suffix max and
+        // min (one load feeds both); decomposed once per sequence
+        const int seqs = g_here * nb * d;
+        for (int q = threadIdx.x; q < 2 * seqs; q += blockDim.x) {
+            const bool fwd = q < seqs;
+            const int r = fwd ? q : q - seqs;
+            const int p = r % d, gb = r / d;  // gb = g * nb + b
+            const int g = gb / nb, b = gb - g * nb;
+            const int i0 = b * k, len = (i0 + k < n ? k : n - i0);
+            const int off = g * nd + i0 * d + p;
+            if (fwd) {
+                const T* x = X + off;
+                T* ox = PX + off;
+                T* on = PN + off;
+                T mx = x[0], mn = mx;
+                ox[0] = mx;
+                on[0] = mn;
+                for (int t = 1; t < len; ++t) {
+                    const T v = x[t * d];
+                    mx = v > mx ? v : mx;  // earliest index wins ties
+                    mn = v < mn ? v : mn;
+                    ox[t * d] = mx;
+                    on[t * d] = mn;
+                }
             } else {
-                ux = SX[a];
-                ln = SN[a];
+                const int last = (len - 1) * d;
+                const T* x = X + off;
+                T* ox = SX + off;
+                T* on = SN + off;
+                T mx = x[last], mn = mx;
+                ox[last] = mx;
+                on[last] = mn;
+                for (int t = last - d; t >= 0; t -= d) {
+                    const T v = x[t];
+                    mx = v >= mx ? v : mx;  // walking backwards: the earlier index wins ties
+                    mn = v <= mn ? v : mn;
+                    ox[t] = mx;
+                    on[t] = mn;
+                }
             }
-            __stcs(du + e, ux);
-            __stcs(dl + e, ln);
         }
+        __syncthreads();
+        // combine, branch-free: consecutive threads -> consecutive elements
+        // (conflict-free shared reads, coalesced streaming stores)
+        for (int g = 0; g < g_here; ++g) {
+            T* du = U + (s0 + g) * nd;
+            T* dl = L + (s0 + g) * nd;
+            const T* pb = PX + g * nd;
+            for (int e = threadIdx.x; e < nd; e += blockDim.x) {
+                const int i = e / d, p = e - i * d;  // compile-time d: multiply-shift
+                const int2 tb = tab[i];
+                const T* pa = pb + tb.x + p;
+                const T* pc = pb + tb.y + p;
+                const T xa = pa[0], xb = pc[0], na = pa[cap], nbv = pc[cap];
+                __stcs(du + e, xb > xa ? xb : xa);  // A is the earlier index: it wins ties
+                __stcs(dl + e, nbv < na ? nbv : na);
+            }
+        }
+        __syncthreads();  // scans and combine done: X and the scan arrays may be reused
+        T* t = X;
+        X = Xn;
+        Xn = t;
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // Sequential prefix sum with first-prefix abandoning (core.py:133-146).
@@ -682,14 +730,15 @@ int series_envelope(int dtype, const void* s, int64_t ns, int n, int d, int w, v
     if (ns <= 0) return TCDTW_OK;
     const int64_t total = ns * (int64_t)n * d;
     const size_t es = dtype == TCDTW_F64 ? 8 : 4;
-    const size_t per_series = (size_t)5 * n * d * es;  // X, prefix max/min, suffix max/min
+    const size_t per_series = (size_t)6 * n * d * es;  // 2 staging + 4 scan arrays
     static const bool naive = getenv("TCDTW_ENV_NAIVE") != nullptr;  // A/B switch
-    if (!naive && per_series <= 48 * 1024) {
-        // ~30-48 KB of staging per block, several blocks per SM so that loads
-        // of one block overlap the compute of the others
-        int G = (int)((36 * 1024) / per_series);
+    if (!naive && per_series + (size_t)8 * n <= 200 * 1024 && n < (1 << 30)) {
+        // ~72 KB per block (3 resident per SM): each keeps one group of
+        // reads in flight while it scans the previous one
+        static const int kb = getenv("TCDTW_ENV_KB") ? atoi(getenv("TCDTW_ENV_KB")) : 54;  // A/B: staging KB (54: best of 18-72)
+        int G = (int)((kb * 1024) / per_series);
         G = G < 1 ? 1 : G;
-        const size_t smem = per_series * G;
+        const size_t smem = per_series * G + (size_t)8 * n;  // + the per-row window table
         int dev = 0, sms = 148, occ = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -698,15 +747,24 @@ int series_envelope(int dtype, const void* s, int64_t ns, int n, int d, int w, v
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
                 return TCDTW_CUDA_ERROR;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
-            int64_t groups = (ns + G - 1) / G;
-            int64_t grid = (int64_t)(occ < 1 ? 1 : occ) * sms * 4;
+            const int64_t groups = (ns + G - 1) / G;
+            int64_t grid = (int64_t)(occ < 1 ? 1 : occ) * sms;
             if (grid > groups) grid = groups;
             kern<<<(int)grid, 256, smem, st>>>(S, ns, n, d, w, G, U, L);
             return launch_status();
         };
+#define TCDTW_ENV_CASE(DD)                                                                             \
+        if (d == DD) {                                                                                 \
+            if (dtype == TCDTW_F64)                                                                    \
+                return go(envelope_stream_kernel<double, DD>, (const double*)s, (double*)u, (double*)l); \
+            return go(envelope_stream_kernel<float, DD>, (const float*)s, (float*)u, (float*)l);       \
+        }
+        TCDTW_ENV_CASE(1) TCDTW_ENV_CASE(2) TCDTW_ENV_CASE(3) TCDTW_ENV_CASE(4) TCDTW_ENV_CASE(5)
+        TCDTW_ENV_CASE(6) TCDTW_ENV_CASE(8) TCDTW_ENV_CASE(20)
+#undef TCDTW_ENV_CASE
         if (dtype == TCDTW_F64)
-            return go(envelope_stream_kernel<double>, (const double*)s, (double*)u, (double*)l);
-        return go(envelope_stream_kernel<float>, (const float*)s, (float*)u, (float*)l);
+            return go(envelope_stream_kernel<double, 0>, (const double*)s, (double*)u, (double*)l);
+        return go(envelope_stream_kernel<float, 0>, (const float*)s, (float*)u, (float*)l);
     }
     const int grid = grid_for(total, 256) > 148 * 64 ? 148 * 64 : grid_for(total, 256);
     if (dtype == TCDTW_F64)

@@ -1865,6 +1865,22 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
     }
 }
 
+// Query row layout of dtw_wave_d_kernel: NV 16-byte vectors (VE elements
+// each) cover the D values; SP = row stride in elements, an odd number of
+// vectors.
+template <typename T, int D>
+struct WaveRow {
+    static constexpr int VE = 16 / (int)sizeof(T);
+    static constexpr int NV = (D + VE - 1) / VE;
+    static constexpr int SPV = NV % 2 == 1 ? NV : NV + 1;
+    static constexpr int SP = SPV * VE;
+    using VT = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+};
+__host__ inline int wave_row_stride(int es, int d) {
+    const int ve = 16 / es, nv = (d + ve - 1) / ve;
+    return (nv % 2 == 1 ? nv : nv + 1) * ve;
+}
+
 // The same wavefront with the dimension count a compile-time constant and a
 // branch-free step: every lane evaluates its cell (inactive lanes on a
 // clamped query row, the result replaced by +inf), lane 0 takes the row above
@@ -1878,7 +1894,11 @@ __global__ void __launch_bounds__(256) dtw_wave_d_kernel(SArgs<T> a, Tiles tl, i
                                                          const uint32_t* __restrict__ cand_of, T* __restrict__ res,
                                                          int* __restrict__ tile_ctr) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int SP = (D % 2 == 1) ? D : D + 1;  // odd word stride: conflict-free column reads
+    // query rows as whole 16-byte vectors, an odd number of them per row:
+    // consecutive lanes read consecutive rows with LDS.128, conflict-free
+    // within each quarter warp
+    constexpr int SP = WaveRow<T, D>::SP;
+    constexpr int VE = WaveRow<T, D>::VE, NV = WaveRow<T, D>::NV;
     const int n = a.n, w = a.w, B = 2 * w + 1;
     const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     T* qs = reinterpret_cast<T*>(smem_raw);                          // (n + 2w) * SP
@@ -1941,9 +1961,27 @@ __global__ void __launch_bounds__(256) dtw_wave_d_kernel(SArgs<T> a, Tiles tl, i
                         up = prow[kc + 1];  // prow[B] = +inf
                         dg = prow[kc];
                     }
-                    int qr = i + k;
+                    int qr = i + k;  // padded query row (INF outside [w, w+n))
                     qr = qr < 0 ? 0 : (qr > qmax ? qmax : qr);
-                    const T* qp = qs + qr * SP;
+                    T qv[NV * VE];
+                    {
+                        using VT = typename WaveRow<T, D>::VT;
+                        const VT* src = reinterpret_cast<const VT*>(qs + qr * SP);
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) {
+                            const VT x = src[v];
+                            if constexpr (VE == 2) {
+                                qv[2 * v] = x.x;
+                                qv[2 * v + 1] = x.y;
+                            } else {
+                                qv[4 * v] = x.x;
+                                qv[4 * v + 1] = x.y;
+                                qv[4 * v + 2] = x.z;
+                                qv[4 * v + 3] = x.w;
+                            }
+                        }
+                    }
+                    const T* qp = qv;
                     T cost;
                     if constexpr (EXACT) {
                         cost = dist_exact<T, D>(rp, qp, D);
@@ -3106,7 +3144,7 @@ static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tile
         kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
         return launch_status();
     }
-    const size_t smem_d = ((size_t)(p.n + 2 * p.w) * ((p.d % 2 == 1) ? p.d : p.d + 1) + (size_t)8 * (p.B + 1)) *
+    const size_t smem_d = ((size_t)(p.n + 2 * p.w) * wave_row_stride((int)sizeof(T), p.d) + (size_t)8 * (p.B + 1)) *
                           sizeof(T);
     auto run_d = [&](auto kern) -> int {
         if (smem_d > 48 * 1024 &&

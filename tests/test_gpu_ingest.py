@@ -75,10 +75,9 @@ def test_report_rows_from_gpu_search(tmp_path):
     # the none rows are the reference's linear scan: no skips
     assert all(r.dtw_skipped == 0 for r in rows if r.method == "none")
     # and the searches behind the rows find the oracle's neighbours
-    idx = ingest.load  # noqa: F841
     import paper_2101_07731_b200 as P
 
-    res = P.SearchIndex(c.values, dtype="f64").search(q.values, P.SearchParams(window=2))
+    res = P.SearchIndex(c.values, dtype="f64").search(q.values, P.SearchParams(window=2, method=P.Method.LB_MV))
     outs, _ = O.nn_search_batch(q.values, c.values, O.make_params(2, "lb_mv"), None, ds.dim_ranges)
     assert [o.best_index for o in outs] == list(res.best_index)
     assert report.main(["--data", str(G / "native_a.txt"), "--method", "lb_mv", "--window", "3", "--reps", "1",
