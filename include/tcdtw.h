@@ -143,7 +143,7 @@ typedef struct tcdtw_search_desc {
     double trigger_ti;
     double trigger_pc;
     double min_cell_frac;
-    int64_t n_queries;      /* queries in this call */
+    int64_t n_queries;      /* queries in this call, 1..65535 */
     int64_t n_candidates;   /* candidates in this shard */
     int64_t candidate_base; /* global index of this shard's candidate 0 */
     int32_t seeds;          /* seed DTWs per query (0 = default 8) */

@@ -1994,10 +1994,14 @@ __global__ void __launch_bounds__(256) dtw_wave_d_kernel(SArgs<T> a, Tiles tl, i
                         }
                         cost = fast_sqrt(s);
                     }
-                    const T best = tmin(tmin(up, dg), mine);
+                    // compare-select minima: the operands are never NaN
+                    // (fmin's NaN handling costs four extra instructions per
+                    // double minimum); equal operands are equal values
+                    const T m1 = dg < up ? dg : up;
+                    const T best = mine < m1 ? mine : m1;
                     T v = EXACT ? add_rn(cost, best) : cost + best;
                     v = act ? v : INF;
-                    rmin = tmin(rmin, v);
+                    rmin = v < rmin ? v : rmin;
                     mine = v;
                     if (act && writer) prow[k] = v;
                 }
@@ -2873,7 +2877,8 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     if (!dsc) return TCDTW_INVALID_INPUT;
     if (dsc->dtype != TCDTW_F32 && dsc->dtype != TCDTW_F64) return TCDTW_INVALID_INPUT;
     if (dsc->n < 1 || dsc->dims < 1 || dsc->dims > kMaxDims || dsc->window < 0) return TCDTW_INVALID_INPUT;
-    if (dsc->n_queries < 1 || dsc->n_candidates < 1 || dsc->n_candidates > 0xfffffff0LL) return TCDTW_INVALID_INPUT;
+    if (dsc->n_queries < 1 || dsc->n_queries > 65535 || dsc->n_candidates < 1 || dsc->n_candidates > 0xfffffff0LL)
+        return TCDTW_INVALID_INPUT;  // queries per call: one compaction grid row each
     if (dsc->method < TCDTW_METHOD_NONE || dsc->method > TCDTW_METHOD_LB_AD) return TCDTW_INVALID_INPUT;
     if (dsc->refresh_period < 1 || dsc->quant_levels < 1 || dsc->max_boxes < 1 || dsc->group_width < 1)
         return TCDTW_INVALID_INPUT;

@@ -19,6 +19,7 @@ import numpy as np
 from . import _dev, _lib
 from .core import METHOD_CODE, InvalidInputError, Method, SearchParams, as_series
 
+MAX_BATCH = 65535  # queries per search call (tcdtw_search_desc.n_queries, include/tcdtw.h)
 TUNE_CANDIDATE_SAMPLE = 23
 TUNE_QUERY_SAMPLE = 8
 
@@ -208,7 +209,7 @@ class SearchIndex:
         if budget_bytes is None:
             free, _ = t.cuda.mem_get_info()
             budget_bytes = int(free * 0.5)
-        lo, hi = 1, max(1, int(n_q))
+        lo, hi = 1, max(1, min(int(n_q), MAX_BATCH))
         if self.workspace_bytes(params, advanced, hi, seeds, reverse_bound) <= budget_bytes:
             return hi
         while lo < hi:
@@ -302,7 +303,7 @@ class SearchIndex:
         n_q = Q.shape[0]
         if batch is None:
             batch = self.auto_batch(params, advanced, n_q, seeds=seeds, reverse_bound=reverse_bound)
-        batch = max(1, min(int(batch), n_q))
+        batch = max(1, min(int(batch), n_q, MAX_BATCH))
         best_idx = t.empty(n_q, dtype=t.int64, device=Q.device)
         best_dist = t.empty(n_q, dtype=t.float64, device=Q.device)
         counters = t.empty((n_q, len(_lib.COUNTERS)), dtype=t.int64, device=Q.device)

@@ -181,3 +181,30 @@ def test_shard_bounds_cover():
             spans = [shard_bounds(n, world, r) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+
+
+def test_new_entry_points_validate_without_gpu():
+    """ABI v2 additions: the reverse-bound flag needs the candidate envelopes;
+    tcdtw_normalize validates shapes and workspace before any launch."""
+    import ctypes
+
+    from paper_2101_07731_b200 import _lib
+
+    L = _lib.load_library()
+    d = _lib.SearchDesc(dtype=0, n=128, dims=6, window=12, method=1, advanced=0, refresh_period=5,
+                        quant_levels=2, max_boxes=6, group_width=6, trigger_ti=0.1, trigger_pc=0.1,
+                        min_cell_frac=1e-5, n_queries=64, n_candidates=10000, candidate_base=0, seeds=0,
+                        flags=_lib.FLAG_REVERSE_LB)
+    out = ctypes.c_size_t()
+    assert L.tcdtw_search_workspace_size(ctypes.byref(d), ctypes.byref(out)) == 1  # no cand_upper/lower
+    d.cand_upper, d.cand_lower = 4096, 8192  # any non-null device addresses: only sizes are computed
+    assert L.tcdtw_search_workspace_size(ctypes.byref(d), ctypes.byref(out)) == 0
+    with_rev = out.value
+    d.flags = 0
+    assert L.tcdtw_search_workspace_size(ctypes.byref(d), ctypes.byref(out)) == 0
+    assert with_rev - out.value >= 64 * 10000 * 4 + 2 * 10000 * 128 * 6 * 4  # (Q,N) bound + planar envelopes
+    nb = ctypes.c_size_t()
+    assert L.tcdtw_normalize_workspace_size(0, ctypes.byref(nb)) == 1
+    assert L.tcdtw_normalize_workspace_size(6, ctypes.byref(nb)) == 0 and nb.value > 0
+    assert L.tcdtw_normalize(None, 10, 6, None, None, None, None, None, 0, None) == 1
+    assert L.tcdtw_normalize(None, 0, 6, None, None, None, None, None, 0, None) == 1
