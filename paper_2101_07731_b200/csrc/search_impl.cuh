@@ -1890,7 +1890,7 @@ __host__ inline int wave_row_stride(int es, int d) {
 // arithmetic plus a few selects (C3: fp64, d = 8).  Row-granular abandoning
 // and the float64 arithmetic order are those of dtw_wave_kernel.
 template <typename T, int D, bool EXACT>
-__global__ void __launch_bounds__(256) dtw_wave_d_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
+__global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
                                                          const uint32_t* __restrict__ cand_of, T* __restrict__ res,
                                                          int* __restrict__ tile_ctr) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -3149,18 +3149,33 @@ static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tile
         kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
         return launch_status();
     }
-    const size_t smem_d = ((size_t)(p.n + 2 * p.w) * wave_row_stride((int)sizeof(T), p.d) + (size_t)8 * (p.B + 1)) *
-                          sizeof(T);
+    // the query rows are shared by the block's warps: pick the block size
+    // (256 / 384 threads, registers capped for two 384-thread blocks) that
+    // keeps the most warps resident
+    const size_t q_bytes = (size_t)(p.n + 2 * p.w) * wave_row_stride((int)sizeof(T), p.d) * sizeof(T);
     auto run_d = [&](auto kern) -> int {
-        if (smem_d > 48 * 1024 &&
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d) != cudaSuccess)
-            return TCDTW_NOT_SUPPORTED;
-        int occ = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem_d);
-        if (occ < 1) return TCDTW_NOT_SUPPORTED;
-        int64_t grid = (int64_t)occ * sms;
+        int best_t = 0, best_w = 0;
+        size_t best_s = 0;
+        static const int force_t = getenv("TCDTW_WAVE_THREADS") ? atoi(getenv("TCDTW_WAVE_THREADS")) : 0;
+        for (int t = 256; t <= 384; t += 128) {
+            if (force_t && t != force_t) continue;
+            const size_t sm = q_bytes + (size_t)(t / 32) * (p.B + 1) * sizeof(T);
+            if (sm > 227 * 1024) continue;
+            if (sm > 48 * 1024 &&
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+                continue;
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, t, sm);
+            if (occ * t / 32 > best_w) {
+                best_w = occ * t / 32;
+                best_t = t;
+                best_s = sm;
+            }
+        }
+        if (best_w < 1) return TCDTW_NOT_SUPPORTED;
+        int64_t grid = (int64_t)(best_w / (best_t / 32)) * sms;
         if (grid > n_tiles) grid = n_tiles;
-        kern<<<(int)grid, 256, smem_d, st>>>(a, tl, n_tiles, cand_of, res, tctr);
+        kern<<<(int)grid, best_t, best_s, st>>>(a, tl, n_tiles, cand_of, res, tctr);
         return launch_status();
     };
     if (!getenv("TCDTW_WAVE_GENERIC")) {  // A/B switch
