@@ -1572,6 +1572,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                 cur[r] = INF;
                 continue;
             }
+            // one FMA chain per cell (two partial sums measured 3% slower on C4)
             float acc = 0.f;
 #pragma unroll
             for (int p = 0; p < D; ++p) {
@@ -3149,14 +3150,15 @@ static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tile
         kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
         return launch_status();
     }
-    // the query rows are shared by the block's warps: pick the block size
-    // (256 / 384 threads, registers capped for two 384-thread blocks) that
-    // keeps the most warps resident
+    // the query rows are shared by the block's warps; block size 256 (or
+    // TCDTW_WAVE_THREADS=384: registers are capped for two such blocks)
     const size_t q_bytes = (size_t)(p.n + 2 * p.w) * wave_row_stride((int)sizeof(T), p.d) * sizeof(T);
     auto run_d = [&](auto kern) -> int {
         int best_t = 0, best_w = 0;
         size_t best_s = 0;
-        static const int force_t = getenv("TCDTW_WAVE_THREADS") ? atoi(getenv("TCDTW_WAVE_THREADS")) : 0;
+        // 384-thread blocks keep 24 warps resident but split each 32-pair
+        // tile unevenly (C3: 2717 vs 3131 q/s at 256): 256 unless overridden
+        static const int force_t = getenv("TCDTW_WAVE_THREADS") ? atoi(getenv("TCDTW_WAVE_THREADS")) : 256;
         for (int t = 256; t <= 384; t += 128) {
             if (force_t && t != force_t) continue;
             const size_t sm = q_bytes + (size_t)(t / 32) * (p.B + 1) * sizeof(T);
