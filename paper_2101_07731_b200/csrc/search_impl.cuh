@@ -3092,12 +3092,68 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
     return a;
 }
 
+// Warp-per-pair wavefront with compile-time d (dtw_wave_d_kernel), or
+// TCDTW_NOT_SUPPORTED for other d.
+template <typename T, int DMAX, bool EXACT>
+static int launch_wave_d(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tiles, const uint32_t* cand_of,
+                         T* res, int* tctr, cudaStream_t st) {
+    const int sms = sm_count();
+    cudaMemsetAsync(tctr, 0, sizeof(int), st);
+    // the query rows are shared by the block's warps; block size 256 (or
+    // TCDTW_WAVE_THREADS=384: registers are capped for two such blocks)
+    const size_t q_bytes = (size_t)(p.n + 2 * p.w) * wave_row_stride((int)sizeof(T), p.d) * sizeof(T);
+    auto run_d = [&](auto kern) -> int {
+        int best_t = 0, best_w = 0;
+        size_t best_s = 0;
+        // 384-thread blocks keep 24 warps resident but split each 32-pair
+        // tile unevenly (C3: 2717 vs 3131 q/s at 256): 256 unless overridden
+        static const int force_t = getenv("TCDTW_WAVE_THREADS") ? atoi(getenv("TCDTW_WAVE_THREADS")) : 256;
+        for (int t = 256; t <= 384; t += 128) {
+            if (force_t && t != force_t) continue;
+            const size_t sm = q_bytes + (size_t)(t / 32) * (p.B + 1) * sizeof(T);
+            if (sm > 227 * 1024) continue;
+            if (sm > 48 * 1024 &&
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+                continue;
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, t, sm);
+            if (occ * t / 32 > best_w) {
+                best_w = occ * t / 32;
+                best_t = t;
+                best_s = sm;
+            }
+        }
+        if (best_w < 1) return TCDTW_NOT_SUPPORTED;
+        int64_t grid = (int64_t)(best_w / (best_t / 32)) * sms;
+        if (grid > n_tiles) grid = n_tiles;
+        kern<<<(int)grid, best_t, best_s, st>>>(a, tl, n_tiles, cand_of, res, tctr);
+        return launch_status();
+    };
+#define TCDTW_WAVE_CASE(DD)                                                                \
+    if (p.d == DD && DD <= DMAX) return run_d(dtw_wave_d_kernel<T, (DD <= DMAX ? DD : 1), EXACT>);
+    TCDTW_WAVE_DIMS(TCDTW_WAVE_CASE)
+#undef TCDTW_WAVE_CASE
+    return TCDTW_NOT_SUPPORTED;
+}
+
+// Few pairs (a small collection or the seed pass of a few queries): the
+// per-pair latency of the lane kernels (one lane walks all n rows) dominates,
+// so the warp-per-pair wavefront (about n + 2W dependent steps) runs instead.
+static inline bool few_pairs(int64_t pairs_upper) {
+    static const bool off = getenv("TCDTW_NO_SMALL_WAVE") != nullptr;  // A/B switch
+    return !off && pairs_upper <= (int64_t)sm_count() * 8;
+}
+
 // DTW launcher over a tile list: thread-per-pair if the band fits the
 // register buckets, else the wavefront kernel.
 template <typename T, int DMAX, bool EXACT>
 static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tiles, const uint32_t* cand_of, T* res,
                       int* tctr, cudaStream_t st) {
     if (n_tiles <= 0) return TCDTW_OK;
+    if (few_pairs(n_tiles * (int64_t)kTile) && !getenv("TCDTW_WAVE_GENERIC")) {
+        const int s = launch_wave_d<T, DMAX, EXACT>(a, p, tl, n_tiles, cand_of, res, tctr, st);
+        if (s != TCDTW_NOT_SUPPORTED) return s;
+    }
     const bool no_lane = getenv("TCDTW_NO_LANE") != nullptr;  // A/B switch for benchmarking
     if constexpr (!EXACT) {
         if (!no_lane && getenv("TCDTW_NO_LANE4") == nullptr) {
@@ -3150,44 +3206,9 @@ static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tile
         kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
         return launch_status();
     }
-    // the query rows are shared by the block's warps; block size 256 (or
-    // TCDTW_WAVE_THREADS=384: registers are capped for two such blocks)
-    const size_t q_bytes = (size_t)(p.n + 2 * p.w) * wave_row_stride((int)sizeof(T), p.d) * sizeof(T);
-    auto run_d = [&](auto kern) -> int {
-        int best_t = 0, best_w = 0;
-        size_t best_s = 0;
-        // 384-thread blocks keep 24 warps resident but split each 32-pair
-        // tile unevenly (C3: 2717 vs 3131 q/s at 256): 256 unless overridden
-        static const int force_t = getenv("TCDTW_WAVE_THREADS") ? atoi(getenv("TCDTW_WAVE_THREADS")) : 256;
-        for (int t = 256; t <= 384; t += 128) {
-            if (force_t && t != force_t) continue;
-            const size_t sm = q_bytes + (size_t)(t / 32) * (p.B + 1) * sizeof(T);
-            if (sm > 227 * 1024) continue;
-            if (sm > 48 * 1024 &&
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
-                continue;
-            int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, t, sm);
-            if (occ * t / 32 > best_w) {
-                best_w = occ * t / 32;
-                best_t = t;
-                best_s = sm;
-            }
-        }
-        if (best_w < 1) return TCDTW_NOT_SUPPORTED;
-        int64_t grid = (int64_t)(best_w / (best_t / 32)) * sms;
-        if (grid > n_tiles) grid = n_tiles;
-        kern<<<(int)grid, best_t, best_s, st>>>(a, tl, n_tiles, cand_of, res, tctr);
-        return launch_status();
-    };
     if (!getenv("TCDTW_WAVE_GENERIC")) {  // A/B switch
-#define TCDTW_WAVE_CASE(DD)                                            \
-        if (p.d == DD && DD <= DMAX) {                                 \
-            const int s = run_d(dtw_wave_d_kernel<T, (DD <= DMAX ? DD : 1), EXACT>); \
-            if (s != TCDTW_NOT_SUPPORTED) return s;                    \
-        }
-        TCDTW_WAVE_DIMS(TCDTW_WAVE_CASE)
-#undef TCDTW_WAVE_CASE
+        const int s = launch_wave_d<T, DMAX, EXACT>(a, p, tl, n_tiles, cand_of, res, tctr, st);
+        if (s != TCDTW_NOT_SUPPORTED) return s;
     }
     const size_t smem = ((size_t)(p.n + 2 * p.w) * ((p.d % 2 == 1) ? p.d : p.d + 1) + (size_t)8 * p.B) * sizeof(T);
     auto kern = dtw_wave_kernel<T, DMAX, EXACT>;
@@ -3355,7 +3376,7 @@ struct SearchImpl {
             // segments, or, when segments are too few to occupy every warp
             // (small collections: C1 has 3 chunks per query), pieces of about
             // survivors / (4 x resident warps), at least 4 pairs per lane
-            if (n_tiles > 0 && laner_rows(a, p.d, p.B) > 0) {
+            if (n_tiles > 0 && laner_rows(a, p.d, p.B) > 0 && !few_pairs(n_tiles * (int64_t)kTile)) {
                 const int64_t surv_est = n_tiles * (int64_t)kTile;
                 const int64_t warps = (int64_t)sms * 16;
                 int seg_len = (int)kChunk;
