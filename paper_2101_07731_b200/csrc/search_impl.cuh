@@ -594,6 +594,22 @@ __global__ void __launch_bounds__(256) compact_write_kernel(const T* __restrict_
     }
 }
 
+// Seeds are already computed: mark their LB entries NaN so the compaction
+// drops them with the bound test alone (!(NaN <= thr)) instead of comparing
+// every (query, candidate) against the query's seed list.  Nothing reads a
+// seed's LB after the seed pass.
+template <typename T>
+__global__ void poison_seeds_kernel(T* __restrict__ lb, int64_t N, int64_t Q, int S,
+                                    const uint32_t* __restrict__ seeds, const int32_t* __restrict__ seed_cnt) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= Q * S) return;
+    const int64_t q = e / S;
+    const int k = (int)(e - q * S);
+    if (k < seed_cnt[q])
+        lb[q * N + seeds[e]] = sizeof(T) == 4 ? (T)__int_as_float(0x7fc00000)                 // quiet NaN
+                                              : (T)__longlong_as_double(0x7ff8000000000000LL);
+}
+
 // per-(chunk, query) survivor segments -> tile counts; then fill
 static __global__ void seg_tiles_count_kernel(int64_t Q, int n_chunks, const int64_t* __restrict__ chunk_off,
                                        int64_t* __restrict__ tile_cnt, int64_t* __restrict__ counters,
@@ -2186,10 +2202,16 @@ __global__ void __launch_bounds__(256) dtw_pipe_kernel(SArgs<T> a, Tiles tl, int
 // One lane per survivor, the tile's query shared by the warp; evaluated only
 // in the trigger band LB_MV > e * d_best (search.py:147).  A survivor whose
 // second bound exceeds thr is marked pruned (res = -1).
+// LB_TI keeps, per lane, the [L, U] intervals of the distances to the window's
+// reference points (the 2W+1 slots) and the column minima; with `ring_smem`
+// those rings live in the warp's shared memory (lane-interleaved, conflict
+// free) instead of global scratch.
 template <typename T, int DMAX, bool EXACT>
 __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
                                                        const uint32_t* __restrict__ cand_of, T* __restrict__ res,
-                                                       T* __restrict__ ti_scratch, int* __restrict__ tile_ctr) {
+                                                       T* __restrict__ ti_scratch, int* __restrict__ tile_ctr,
+                                                       bool ring_smem) {
+    extern __shared__ __align__(16) unsigned char adv_smem[];
     const int n = a.n, d = a.d, w = a.w, B = 2 * w + 1;
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -2268,7 +2290,8 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
         } else {
             // LB_TI, TIP_TOP variant (search.py:150-153), lb_ti.py:140-200.
             // Slot rings of size B per lane, interleaved by lane in scratch.
-            T* lo_r = ti_scratch + gwarp * 3 * (int64_t)B * 32;
+            T* lo_r = ring_smem ? reinterpret_cast<T*>(adv_smem) + (threadIdx.x >> 5) * 3 * (int64_t)B * 32
+                                : ti_scratch + gwarp * 3 * (int64_t)B * 32;
             T* up_r = lo_r + (int64_t)B * 32;
             T* cm_r = up_r + (int64_t)B * 32;
             const T* qst = a.qsteps + q * (int64_t)(n - 1);
@@ -3323,8 +3346,15 @@ struct SearchImpl {
         dim3 cgrid((unsigned)p.n_chunks, (unsigned)p.Q);
         if (p.Q > 65535) return TCDTW_INVALID_INPUT;
         const T* lb2 = p.rev ? at<T>(ws, p.o_lb2) : nullptr;
+        int S_c = p.S;  // seeds compared per element (none once poisoned)
+        if (p.has_lb && p.S > 0) {
+            poison_seeds_kernel<T><<<grid_for(p.Q * p.S, 256), 256, 0, st>>>(
+                const_cast<T*>(a.lb), p.N, p.Q, p.S, at<uint32_t>(ws, p.o_seed), at<int32_t>(ws, p.o_seedcnt));
+            TRY(launch_status());
+            S_c = 0;
+        }
         compact_count_kernel<T><<<cgrid, 256, 0, st>>>(a.lb, lb2, p.N, p.n_chunks, a.dbest, a.mg, all,
-                                                       at<uint32_t>(ws, p.o_seed), at<int32_t>(ws, p.o_seedcnt), p.S,
+                                                       at<uint32_t>(ws, p.o_seed), at<int32_t>(ws, p.o_seedcnt), S_c,
                                                        ccnt);
         TRY(launch_status());
         cudaMemsetAsync(ccnt + p.Q * p.n_chunks, 0, 8, st);
@@ -3335,7 +3365,7 @@ struct SearchImpl {
         uint32_t* surv = at<uint32_t>(ws, p.o_surv);
         T* res = at<T>(ws, p.o_res);
         compact_write_kernel<T><<<cgrid, 256, 0, st>>>(a.lb, lb2, p.N, p.n_chunks, a.dbest, a.mg, all,
-                                                       at<uint32_t>(ws, p.o_seed), at<int32_t>(ws, p.o_seedcnt), p.S,
+                                                       at<uint32_t>(ws, p.o_seed), at<int32_t>(ws, p.o_seedcnt), S_c,
                                                        coff, surv, res);
         TRY(launch_status());
         int64_t* tcnt = at<int64_t>(ws, p.o_tcnt);
@@ -3364,8 +3394,15 @@ struct SearchImpl {
             if (sa == TCDTW_NOT_SUPPORTED) {
                 cudaMemsetAsync(at<int>(ws, p.o_tctr), 0, sizeof(int), st);
                 int grid = (p.adv_warps * 32) / 256;
-                advanced_kernel<T, DMAX, EXACT><<<grid, 256, 0, st>>>(a, tl, n_tiles, surv, res, at<T>(ws, p.o_tisc),
-                                                                     at<int>(ws, p.o_tctr));
+                // LB_TI: slot rings in shared memory when 8 warps' rings fit
+                const size_t ring = (size_t)8 * 3 * p.B * 32 * sizeof(T);
+                bool rs = a.adv == TCDTW_METHOD_LB_TI && ring <= 200 * 1024 && !getenv("TCDTW_TI_GLOBAL_RING");
+                auto kern = advanced_kernel<T, DMAX, EXACT>;
+                if (rs && ring > 48 * 1024 &&
+                    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring) != cudaSuccess)
+                    rs = false;
+                kern<<<grid, 256, rs ? ring : 0, st>>>(a, tl, n_tiles, surv, res, at<T>(ws, p.o_tisc),
+                                                       at<int>(ws, p.o_tctr), rs);
                 sa = launch_status();
             }
             TRY(sa);
