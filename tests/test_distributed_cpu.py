@@ -59,7 +59,19 @@ def _worker(rank, world, port, q):
         q.put((rank, repr(e)))
 
 
-@pytest.mark.parametrize("world", [2])
+def test_shard_bounds_partition():
+    from paper_2101_07731_b200.distributed import shard_bounds
+
+    for n in (1, 7, 1000, 1_000_000):
+        for world in (1, 2, 3, 4, 8):
+            b = [shard_bounds(n, world, r) for r in range(world)]
+            assert b[0][0] == 0 and b[-1][1] == n
+            assert all(b[r][1] == b[r + 1][0] for r in range(world - 1))
+            sizes = [e - s for s, e in b]
+            assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("world", [2, 3])
 def test_combine_and_exchange_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
