@@ -14,7 +14,15 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/f
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/fin_launches.csv python bench.py --steps 1 --warmup 1 --queries 1000 --no-cpu-baseline > gpurun_out/fin_launches.log 2>&1
 echo "launches exit=$?" >> gpurun_out/fin_launches.log
 CMD="python bench.py --steps 1 --warmup 1 --queries 256 --candidates 200000 --no-cpu-baseline"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"dtw_laner" -s 1 -c 1 -o gpurun_out/fin_laner $CMD > gpurun_out/fin_ncu_laner.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"lbmv_matrix" -s 0 -c 1 -o gpurun_out/fin_lbmv $CMD > gpurun_out/fin_ncu_lbmv.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"envelope_stream" -s 0 -c 1 -o gpurun_out/fin_env $CMD > gpurun_out/fin_ncu_env.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"dtw_wave_d" -s 1 -c 1 -o gpurun_out/fin_c3 python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/fin_ncu_c3.log 2>&1
+# full captures are summarised on the box (the .ncu-rep files would exceed
+# gpurun's 64 MiB copy-back limit) and then deleted
+cap() {  # name, kernel regex, launch skip, command...
+  local name=$1 rx=$2 skip=$3; shift 3
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $skip -c 1 -o gpurun_out/$name "$@" > gpurun_out/${name}.log 2>&1
+  python scripts/summarize_ncu.py full gpurun_out/$name.ncu-rep "$* (-k $rx -s $skip -c 1)" > gpurun_out/${name}_summary.txt 2>&1
+  rm -f gpurun_out/$name.ncu-rep
+}
+cap fin_laner dtw_laner 1 $CMD
+cap fin_lbmv lbmv_matrix 0 $CMD
+cap fin_env envelope_stream 0 $CMD
+cap fin_c3 dtw_wave_d 1 python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline
