@@ -205,7 +205,7 @@ def test_c1a_full_parity(P):
 
 
 def test_c1b_parity(P):
-    _oracle_check(P, "C1", 1, 64, rel=0.0)
+    _oracle_check(P, "C1", 1, 128, rel=0.0)
 
 
 def test_c1_cascades_parity(P):
@@ -214,15 +214,15 @@ def test_c1_cascades_parity(P):
 
 
 def test_c2_parity(P):
-    _oracle_check(P, "C2", 0, 16, rel=0.0)
+    _oracle_check(P, "C2", 0, 48, rel=0.0)
 
 
 def test_c3_parity(P):
-    _oracle_check(P, "C3", 0, 8, rel=0.0)
+    _oracle_check(P, "C3", 0, 24, rel=0.0)
 
 
 def test_c4_sampled_parity(P):
-    _oracle_check(P, "C4", 0, 4, rel=0.0)
+    _oracle_check(P, "C4", 0, 16, rel=0.0)
 
 
 # ------------------------------------------------------------- edge cases
