@@ -353,3 +353,21 @@ def test_tc_dtw_select_and_tune(P):
     for q, ref in zip(queries, base):
         out = P.nn_search(q, cands, tuned, advanced=choice)
         assert (out.best_index, out.best_distance) == (ref.best_index, ref.best_distance)
+
+
+def test_gpu_cost_selection(P):
+    """Row f1: selection and tuning ranked by measured GPU phase times
+    (metric="time") instead of the work model; answers never change."""
+    rng = np.random.default_rng(11)
+    series = np.cumsum(rng.normal(size=(40, 32, 3)), axis=1)
+    queries, cands = list(series[:6]), list(series[6:])
+    params = P.SearchParams(window=4, method="tc_dtw")
+    choice = P.tc_dtw_select(queries, cands, params, metric="time")
+    assert choice in (P.Method.LB_TI, P.Method.LB_PC)
+    log = []
+    tuned = P.tune_params(queries, cands, params, seed=1, metric="time", log=log)
+    assert len(log) == 7 and all(cost > 0 for _, _, cost in log)
+    for q in queries:
+        ref = P.nn_search(q, cands, P.SearchParams(window=4, method="none"))
+        out = P.nn_search(q, cands, tuned, advanced=choice)
+        assert (out.best_index, out.best_distance) == (ref.best_index, ref.best_distance)
