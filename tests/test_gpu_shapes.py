@@ -1,0 +1,38 @@
+"""Search parity over a spread of shapes, so that every DTW kernel the
+dispatcher can pick (R-row lane kernel for its compiled shapes, two-row lane
+kernel, thread-per-pair, compile-time-d wavefront, generic wavefront,
+few-pairs path) is checked against the oracle, in float32 and float64."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [  # (n, d, W)
+    (1, 3, 0), (2, 1, 1), (7, 2, 3), (16, 4, 6), (33, 7, 5), (64, 20, 6), (64, 6, 12), (100, 9, 10),
+    (128, 6, 12), (128, 5, 51), (128, 3, 6), (128, 8, 12), (200, 12, 40), (64, 32, 3), (96, 16, 30),
+    (256, 5, 12), (130, 6, 12), (48, 24, 48),
+]
+
+
+@pytest.mark.parametrize("n,d,w", SHAPES)
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_search_shapes(n, d, w, dtype):
+    import paper_2101_07731_b200 as P
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(n * 1000 + d * 10 + w)
+    N, Q = 900, 5
+    X = np.cumsum(rng.normal(size=(N + Q, n, d)), axis=1)
+    X = (X - X.reshape(-1, d).mean(0)) / (X.reshape(-1, d).std(0) + 1e-12)
+    np_t = np.float32 if dtype == "f32" else np.float64
+    X = X.astype(np_t)
+    cands, qs = X[:N], X[N:]
+    res = P.SearchIndex(cands, dtype=dtype).search(qs, P.SearchParams(window=w, method=P.Method.LB_MV))
+    outs, _ = O.nn_search_batch(qs.astype(np.float64), cands.astype(np.float64), O.make_params(w, "lb_mv"), None,
+                                None)
+    for i, o in enumerate(outs):
+        assert res.best_index[i] == o.best_index, (n, d, w, dtype, i)
+        assert res.best_distance[i] == o.best_distance, (n, d, w, dtype, i)
+    c = res.counters
+    assert np.all(c["dtw_computed"] + c["dtw_skipped"] == N)
