@@ -1906,7 +1906,9 @@ __host__ inline int wave_row_stride(int es, int d) {
 // (runtime d: address arithmetic, guards, reconvergence) to the DP's own
 // arithmetic plus a few selects (C3: fp64, d = 8).  Row-granular abandoning
 // and the float64 arithmetic order are those of dtw_wave_kernel.
-template <typename T, int D, bool EXACT>
+// QG: the query is read from global memory (L1) instead of being staged --
+// series too long for the staged rows to fit in shared memory.
+template <typename T, int D, bool EXACT, bool QG = false>
 __global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
                                                          const uint32_t* __restrict__ cand_of, T* __restrict__ res,
                                                          int* __restrict__ tile_ctr) {
@@ -1919,7 +1921,7 @@ __global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
     const int n = a.n, w = a.w, B = 2 * w + 1;
     const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     T* qs = reinterpret_cast<T*>(smem_raw);                          // (n + 2w) * SP
-    T* prow = qs + (size_t)(n + 2 * w) * SP + (size_t)wib * (B + 1);  // per warp: B + 1 (last = +inf)
+    T* prow = qs + (QG ? (size_t)0 : (size_t)(n + 2 * w) * SP) + (size_t)wib * (B + 1);  // per warp: B + 1 (last = +inf)
     __shared__ int64_t tile_s;
     const T INF = dev_inf<T>();
     const unsigned FULL = 0xffffffffu;
@@ -1934,7 +1936,7 @@ __global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
         const int64_t q = tl.q[tile];
         const int64_t e0 = tl.begin[tile];
         const int len = tl.len[tile];
-        if (q != cached_q) {
+        if (!QG && q != cached_q) {
             const T* qsrc = a.queries + q * (int64_t)n * D;
             for (int e = threadIdx.x; e < (n + 2 * w) * D; e += blockDim.x) {
                 const int r = e / D, p = e - (e / D) * D;
@@ -1981,7 +1983,13 @@ __global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
                     int qr = i + k;  // padded query row (INF outside [w, w+n))
                     qr = qr < 0 ? 0 : (qr > qmax ? qmax : qr);
                     T qv[NV * VE];
-                    {
+                    if constexpr (QG) {
+                        const int col = i + k - w;
+                        const bool in = (unsigned)col < (unsigned)n;
+                        const T* src = a.queries + ((int64_t)q * n + (in ? col : 0)) * D;
+#pragma unroll
+                        for (int p = 0; p < D; ++p) qv[p] = in ? __ldg(src + p) : INF;
+                    } else {
                         using VT = typename WaveRow<T, D>::VT;
                         const VT* src = reinterpret_cast<const VT*>(qs + qr * SP);
 #pragma unroll
@@ -3152,8 +3160,26 @@ static int launch_wave_d(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_t
         kern<<<(int)grid, best_t, best_s, st>>>(a, tl, n_tiles, cand_of, res, tctr);
         return launch_status();
     };
-#define TCDTW_WAVE_CASE(DD)                                                                \
-    if (p.d == DD && DD <= DMAX) return run_d(dtw_wave_d_kernel<T, (DD <= DMAX ? DD : 1), EXACT>);
+    // staged query rows too large for shared memory: read them through L1
+    const bool qg = q_bytes + (size_t)8 * (p.B + 1) * sizeof(T) > 227 * 1024;
+#define TCDTW_WAVE_CASE(DD)                                                                           \
+    if (p.d == DD && DD <= DMAX) {                                                                    \
+        if (qg) {                                                                                     \
+            auto kq = dtw_wave_d_kernel<T, (DD <= DMAX ? DD : 1), EXACT, true>;                       \
+            const size_t sm = (size_t)8 * (p.B + 1) * sizeof(T);                                      \
+            if (sm > 48 * 1024 &&                                                                     \
+                cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) \
+                return TCDTW_NOT_SUPPORTED;                                                           \
+            int occ = 0;                                                                              \
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kq, 256, sm);                         \
+            if (occ < 1) return TCDTW_NOT_SUPPORTED;                                                  \
+            int64_t grid = (int64_t)occ * sms;                                                        \
+            if (grid > n_tiles) grid = n_tiles;                                                       \
+            kq<<<(int)grid, 256, sm, st>>>(a, tl, n_tiles, cand_of, res, tctr);                       \
+            return launch_status();                                                                   \
+        }                                                                                             \
+        return run_d(dtw_wave_d_kernel<T, (DD <= DMAX ? DD : 1), EXACT>);                             \
+    }
     TCDTW_WAVE_DIMS(TCDTW_WAVE_CASE)
 #undef TCDTW_WAVE_CASE
     return TCDTW_NOT_SUPPORTED;
@@ -3486,8 +3512,15 @@ struct SearchImpl {
                                                      n_tiles > 0 ? done_list : nullptr, done_cnt, p.done_cap, surv,
                                                      res, minv, dbi, F);
         TRY(launch_status());
-        fin_rescore_warp_kernel<T, DMAX><<<sms * 4, 256, (size_t)8 * (2 * p.w + 1) * sizeof(double), st>>>(a, F, min64);
-        TRY(launch_status());
+        {
+            const size_t fsm = (size_t)8 * (2 * p.w + 1) * sizeof(double);  // one float64 band row per warp
+            if (fsm > 48 * 1024 &&
+                cudaFuncSetAttribute(fin_rescore_warp_kernel<T, DMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)fsm) != cudaSuccess)
+                return TCDTW_NOT_SUPPORTED;
+            fin_rescore_warp_kernel<T, DMAX><<<sms * 4, 256, fsm, st>>>(a, F, min64);
+            TRY(launch_status());
+        }
         // survivors' completed list overflowed: scan every tile instead
         if (n_tiles > 0) {
             fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, tl, n_tiles, surv, res, minv, dbi, EXACT ? 1 : 0,

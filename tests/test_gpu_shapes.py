@@ -36,3 +36,21 @@ def test_search_shapes(n, d, w, dtype):
         assert res.best_distance[i] == o.best_distance, (n, d, w, dtype, i)
     c = res.counters
     assert np.all(c["dtw_computed"] + c["dtw_skipped"] == N)
+
+
+@pytest.mark.parametrize("n,d,w,dtype", [(4096, 8, 409, "f64"), (4096, 6, 409, "f32"), (2048, 3, 1000, "f64")])
+def test_long_series(n, d, w, dtype):
+    """Series whose staged query rows exceed shared memory: the wavefront
+    reads them through L1; wide bands: the float64 re-score's band rows."""
+    import paper_2101_07731_b200 as P
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(n + d + w)
+    N, Q = 40, 2
+    X = np.cumsum(rng.normal(size=(N + Q, n, d)), axis=1)
+    X = ((X - X.reshape(-1, d).mean(0)) / X.reshape(-1, d).std(0)).astype(np.float32 if dtype == "f32" else np.float64)
+    res = P.SearchIndex(X[:N], dtype=dtype).search(X[N:], P.SearchParams(window=w, method=P.Method.LB_MV))
+    outs, _ = O.nn_search_batch(X[N:].astype(np.float64), X[:N].astype(np.float64), O.make_params(w, "lb_mv"),
+                                None, None)
+    assert list(res.best_index) == [o.best_index for o in outs]
+    assert list(res.best_distance) == [o.best_distance for o in outs]
