@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--window-index", type=int, default=0)
-    ap.add_argument("--method", default="lb_mv")
+    ap.add_argument("--method", default="lb_mv", help="a Method value, or auto (GPU-cost choice, SURVEY 8f f1)")
     ap.add_argument("--queries", type=int, default=0, help="use only the first Q queries (0 = all)")
     ap.add_argument("--candidates", type=int, default=0, help="override N_c (0 = config)")
     ap.add_argument("--batch", type=int, default=0)
@@ -214,6 +214,12 @@ def cpu_queries_per_sec(wl, w, method, advanced, n_queries_hint, budget_s, threa
 def resolve_method(P, wl, w, method, dim_range):
     """The reference CLI's setup stage (cli.py:228-235): tune_params and,
     for tc_dtw, tc_dtw_select on the seeded sample; untimed."""
+    if method == "auto":  # GPU-cost choice among LB_MV / TC-DTW(LB_PC) / TC-DTW(LB_TI) (row f1)
+        base = P.tune_params(list(wl.queries[:64].astype(np.float64)), list(wl.candidates[:4096].astype(np.float64)),
+                             P.SearchParams(window=w, method=P.Method.TC_DTW), seed=0, dim_range=dim_range,
+                             metric="time")
+        return P.select_method(list(wl.queries[:64].astype(np.float64)),
+                               list(wl.candidates[:4096].astype(np.float64)), base, dim_range=dim_range)
     params = P.SearchParams(window=w, method=P.Method(method))
     advanced = None
     if params.method == P.Method.TC_DTW:
@@ -239,6 +245,8 @@ def run_reference(args):
     wl = make_workload(args.config, n_candidates=args.candidates or None, n_queries=args.queries or None)
     w = wl.spec.windows()[args.window_index]
     method, advanced = args.method, None
+    if method == "auto":  # the reference has no GPU-cost choice: its classic bound
+        method = "lb_mv"
     if method == "tc_dtw":
         advanced = os.environ.get("TCDTW_REF_ADVANCED", "lb_pc")  # the GPU arm's tc_dtw_select pick on C4
     del core

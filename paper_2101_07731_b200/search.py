@@ -395,6 +395,27 @@ def tc_dtw_select(sample_queries, sample_candidates, params: SearchParams, dim_r
     return Method.LB_TI if cost_ti < cost_pc else Method.LB_PC
 
 
+def select_method(sample_queries, sample_candidates, params: SearchParams, dim_range=None) -> tuple:
+    """GPU-cost method choice (an extension of
+    tc_dtw_select): time LB_MV alone, TC-DTW with LB_TI and TC-DTW with LB_PC
+    on the sample with the search's CUDA-event phase times and return the
+    fastest as (params, advanced).  On the GPU the second bound often costs
+    more than the DTW work it removes, a case the
+    reference's two-way choice cannot express.  Ties go to the simpler
+    method (LB_MV, then LB_PC)."""
+    if not sample_queries or not sample_candidates:
+        raise InvalidInputError("selection sample is empty")
+    options = [(replace(params, method=Method.LB_MV), None),
+               (replace(params, method=Method.TC_DTW), Method.LB_PC),
+               (replace(params, method=Method.TC_DTW), Method.LB_TI)]
+    best, best_cost = None, None
+    for p, adv in options:
+        cost = _run_sample(sample_queries, sample_candidates, p, adv, dim_range, "time")
+        if best_cost is None or cost < best_cost:
+            best, best_cost = (p, adv), cost
+    return best
+
+
 def tune_params(queries, candidates, params: SearchParams, grids: dict | None = None, seed: int = 0,
                 dim_range=None, metric: str = "work", log: list | None = None) -> SearchParams:
     """Grid-search trigger thresholds and quantisation level on a seeded

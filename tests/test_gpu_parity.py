@@ -371,3 +371,18 @@ def test_gpu_cost_selection(P):
         ref = P.nn_search(q, cands, P.SearchParams(window=4, method="none"))
         out = P.nn_search(q, cands, tuned, advanced=choice)
         assert (out.best_index, out.best_distance) == (ref.best_index, ref.best_distance)
+
+
+def test_select_method_gpu_cost(P):
+    """Row f1 extension: the fastest of LB_MV / TC-DTW(LB_PC) / TC-DTW(LB_TI)
+    by measured GPU time; the chosen configuration finds the same answers."""
+    rng = np.random.default_rng(3)
+    series = np.cumsum(rng.normal(size=(60, 48, 3)), axis=1)
+    queries, cands = list(series[:6]), list(series[6:])
+    params, adv = P.select_method(queries, cands, P.SearchParams(window=5))
+    assert (params.method, adv) in ((P.Method.LB_MV, None), (P.Method.TC_DTW, P.Method.LB_PC),
+                                    (P.Method.TC_DTW, P.Method.LB_TI))
+    for q in queries:
+        ref = P.nn_search(q, cands, P.SearchParams(window=5, method="none"))
+        out = P.nn_search(q, cands, params, advanced=adv)
+        assert (out.best_index, out.best_distance) == (ref.best_index, ref.best_distance)
