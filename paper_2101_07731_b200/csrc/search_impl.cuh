@@ -665,6 +665,7 @@ struct SArgs {
     unsigned long long* done_cnt;
     int64_t done_cap;
     int refill_min;  // lane kernel: refill once at least this many lanes are free
+    int thr_every;   // lane kernels: re-read the live d_best every this many rows
     // float32: queries as coordinate pairs with W INF columns before and
     // W + 8 after, (Q, qpad_rows, (d+1)/2) float2, staged by the R-row lane kernel
     const float2* qpad;
@@ -1687,7 +1688,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
 #pragma unroll
                 for (int u = 0; u < RD; ++u) c[u] = nc[u];
                 since += R;
-                if (since >= 8) {
+                if (since >= a.thr_every) {
                     since = 0;
                     thr = scale_up<float>(thr_pend_raw, a.mg.prune);
                     if (a.abandon) thr_pend_raw = load_volatile(a.dbest + cq);
@@ -3114,6 +3115,7 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
     }
     a.abandon = dsc->method != TCDTW_METHOD_NONE;
     a.refill_min = 8;
+    a.thr_every = getenv("TCDTW_THR_EVERY") ? atoi(getenv("TCDTW_THR_EVERY")) : 8;
     if (const char* rm = getenv("TCDTW_REFILL_MIN")) a.refill_min = atoi(rm);
     a.done_list = nullptr;  // set for the survivors pass only
     a.done_cnt = nullptr;
