@@ -218,15 +218,69 @@ const char *tcdtw_dtw_kernel_name(const tcdtw_search_desc *desc);
 /* Device-side ingest.                                   */
 /* ---------------------------------------------------------------------- */
 
+/* Text datasets -> host float64 values.  Replaces the
+ * tokenizing and float() conversion of parse_native (ingest.py:92-126) and
+ * parse_ts_subset (ingest.py:157-231); the caller reads the file and turns
+ * the error record into the reference's ParseError message (ingest.py in
+ * this package).  `text`/`values` are HOST pointers.
+ *   values == NULL : validate the layout and report the shape in *info
+ *                    (native: header and line count; .ts: the whole file);
+ *   values != NULL : also convert into values (num_series, length, dims),
+ *                    NaN for missing tokens (NA / NaN / ?), capacity in
+ *                    doubles.
+ * Returns TCDTW_OK, TCDTW_INVALID_INPUT with info->error set, or
+ * TCDTW_WORKSPACE_TOO_SMALL.  Lines are numbered from 1 as the reference
+ * numbers them (universal newlines). */
+enum tcdtw_text_format { TCDTW_FORMAT_NATIVE = 0, TCDTW_FORMAT_TS = 1 };
+
+enum tcdtw_parse_error {
+    TCDTW_PARSE_OK = 0,
+    TCDTW_PARSE_EMPTY,            /* "empty file" */
+    TCDTW_PARSE_HEADER_FIELDS,    /* header is not three fields */
+    TCDTW_PARSE_HEADER_INT,       /* non-integer header field */
+    TCDTW_PARSE_HEADER_POSITIVE,  /* header fields must be positive */
+    TCDTW_PARSE_LINE_COUNT,       /* expected/found value lines */
+    TCDTW_PARSE_ROW_WIDTH,        /* expected/found values on a line */
+    TCDTW_PARSE_TOKEN,            /* non-numeric token (tok_off, tok_len) */
+    TCDTW_PARSE_TS_AFTER_DATA,    /* directive after @data */
+    TCDTW_PARSE_TS_DIRECTIVE,     /* unsupported directive (tok = its name) */
+    TCDTW_PARSE_TS_FLAG,          /* expected true/false (tok = the argument) */
+    TCDTW_PARSE_TS_TIMESTAMPS,    /* timestamped files are not supported */
+    TCDTW_PARSE_TS_UNEQUAL,       /* unequal-length series are not supported */
+    TCDTW_PARSE_TS_INT_ARG,       /* @dimensions / @seriesLength argument is not an int */
+    TCDTW_PARSE_TS_BEFORE_DATA,   /* data before @data directive */
+    TCDTW_PARSE_TS_LABEL,         /* missing class label */
+    TCDTW_PARSE_TS_DIMS,          /* expected/found dimensions */
+    TCDTW_PARSE_TS_RAGGED,        /* ragged dimensions within one series */
+    TCDTW_PARSE_TS_LENGTH,        /* expected/found length */
+    TCDTW_PARSE_TS_SHAPE,         /* series shape differs from earlier series */
+    TCDTW_PARSE_TS_NO_DATA        /* no data lines */
+};
+
+typedef struct tcdtw_parse_info {
+    int64_t num_series, length, dims; /* shape on success */
+    int64_t line;                     /* 1-based line of the error (0 = whole file) */
+    int64_t tok_off, tok_len;         /* offending token's byte range in text (-1 = none) */
+    int64_t expected, found;          /* counts of the count/shape errors */
+    int64_t name_off, name_len;       /* .ts @problemName argument (-1 = none) */
+    int32_t error;                    /* tcdtw_parse_error */
+    int32_t reserved;
+} tcdtw_parse_info;
+
+int tcdtw_parse_text(int32_t format, const char *text, size_t len, double *values, int64_t capacity,
+                     tcdtw_parse_info *info);
+
 /* normalize(ds) -> Dataset(values, dim_ranges), ingest.py:245-261, on the
- * device: values (n_points, dims) float64 with NaN marking missing entries
- * (n_points = num_series * length); out (n_points, dims) z-normalised per
- * dimension with the population mean/std over all points (missing values
- * enter as raw zeros, zero-variance dimensions become all-zeros); mean, std,
- * range (dims,) -- range is the post-normalisation max - min
- * (ingest.py:235-237), the LB_PC dim_range.  Deterministic tree reductions:
- * statistics equal the reference's to rounding.  out may alias values. */
-int tcdtw_normalize_workspace_size(int32_t dims, size_t *bytes);
+ * device, bit-identical to the reference: values (n_points, dims) float64
+ * with NaN marking missing entries (n_points = num_series * length); out
+ * (n_points, dims) z-normalised per dimension with the population mean/std
+ * over all points (missing values enter as raw zeros, zero-variance
+ * dimensions become all-zeros); mean, std, range (dims,) -- range is the
+ * post-normalisation max - min (ingest.py:235-237), the LB_PC dim_range.
+ * The sums follow numpy's axis-0 reduction order: a sequential running sum
+ * per dimension for dims >= 2, numpy's pairwise summation for dims == 1.
+ * out may alias values. */
+int tcdtw_normalize_workspace_size(int64_t n_points, int32_t dims, size_t *bytes);
 int tcdtw_normalize(const double *values, int64_t n_points, int32_t dims, double *out, double *mean,
                     double *std, double *range, void *workspace, size_t ws_bytes, void *stream);
 

@@ -47,6 +47,13 @@ class SearchDesc(ctypes.Structure):
     ]
 
 
+class ParseInfo(ctypes.Structure):
+    """tcdtw_parse_info (include/tcdtw.h)."""
+
+    _fields_ = [(f, _i64) for f in ("num_series", "length", "dims", "line", "tok_off", "tok_len", "expected", "found",
+                                    "name_off", "name_len")] + [("error", _i32), ("reserved", _i32)]
+
+
 _SIGS = {
     "tcdtw_strerror": ([ctypes.c_int], ctypes.c_char_p),
     "tcdtw_abi_version": ([], ctypes.c_int),
@@ -63,7 +70,8 @@ _SIGS = {
                               _vp, _vp, _vp, _vp], ctypes.c_int),
     "tcdtw_lb_pc": ([ctypes.c_int, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
                     ctypes.c_int),
-    "tcdtw_normalize_workspace_size": ([_i32, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "tcdtw_parse_text": ([_i32, ctypes.c_char_p, ctypes.c_size_t, _vp, _i64, ctypes.POINTER(ParseInfo)], ctypes.c_int),
+    "tcdtw_normalize_workspace_size": ([_i64, _i32, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "tcdtw_normalize": ([_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp], ctypes.c_int),
     "tcdtw_search_workspace_size": ([ctypes.POINTER(SearchDesc), ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "tcdtw_search_seed": ([ctypes.POINTER(SearchDesc), _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp], ctypes.c_int),

@@ -34,7 +34,7 @@ int search_finish(const tcdtw_search_desc*, const void*, const void*, const void
 int lb_mv_matrix(int, const void*, const void*, const void*, int64_t, int64_t, int, int, void*, cudaStream_t);
 int alu_probe(int, int, int, void*, double*, cudaStream_t);
 const char* dtw_kernel_name(const tcdtw_search_desc*);
-size_t normalize_workspace_bytes(int);
+size_t normalize_workspace_bytes(int64_t, int);
 int normalize_f64(const double*, int64_t, int, double*, double*, double*, double*, double*, cudaStream_t);
 }  // namespace tcdtw
 
@@ -60,7 +60,7 @@ const char* tcdtw_strerror(int status) {
     }
 }
 
-int tcdtw_abi_version(void) { return 2; }
+int tcdtw_abi_version(void) { return 3; }  // 3: tcdtw_parse_text, normalize workspace by size
 
 unsigned long long tcdtw_launch_count(void) { return g_launches.load(); }
 
@@ -193,17 +193,17 @@ int tcdtw_alu_probe(int dtype, int32_t blocks, int32_t iters, void* sink, double
 }
 
 
-int tcdtw_normalize_workspace_size(int32_t dims, size_t* bytes) {
-    if (dims < 1 || dims > kMaxDims || !bytes) return TCDTW_INVALID_INPUT;
-    *bytes = normalize_workspace_bytes(dims);
+int tcdtw_normalize_workspace_size(int64_t n_points, int32_t dims, size_t* bytes) {
+    if (n_points < 1 || dims < 1 || !bytes) return TCDTW_INVALID_INPUT;
+    *bytes = normalize_workspace_bytes(n_points, dims);
     return TCDTW_OK;
 }
 
 int tcdtw_normalize(const double* values, int64_t n_points, int32_t dims, double* out, double* mean, double* std_,
                     double* range, void* workspace, size_t ws_bytes, void* stream) {
-    if (n_points < 1 || dims < 1 || dims > kMaxDims) return TCDTW_INVALID_INPUT;  // ingest.py:62-63
+    if (n_points < 1 || dims < 1) return TCDTW_INVALID_INPUT;  // ingest.py:62-63
     if (!values || !out || !mean || !std_ || !range) return TCDTW_INVALID_INPUT;
-    if (!workspace || ws_bytes < normalize_workspace_bytes(dims)) return TCDTW_WORKSPACE_TOO_SMALL;
+    if (!workspace || ws_bytes < normalize_workspace_bytes(n_points, dims)) return TCDTW_WORKSPACE_TOO_SMALL;
     return normalize_f64(values, n_points, dims, out, mean, std_, range, (double*)workspace, S(stream));
 }
 }  // extern "C"

@@ -1,30 +1,23 @@
 """Benchmark report rows in the reference's schema.
 
-The reference's benchmark layer (cli.py:36-39 CSV_COLUMNS, RunReport
-cli.py:46-83, run_benchmark cli.py:165-212, _run_cell cli.py:226-271,
-emit_report cli.py:294-321) reports, for every (dataset, method, window,
-dims) cell, the skip rate and the speedup against the plain windowed-DTW scan
-(method none).  This module produces the same rows from the GPU search --
-the same columns, the same rounding, the same csv / json / table renderings
--- so GPU rows can be set next to the reference's CPU rows.  Counters come
-from the GPU cascade (order-free, so skip counts may differ from the
-reference's; the nearest neighbours do not), times from the batched search:
-``lb_time_s`` / ``dtw_time_s`` from the CUDA-event phase times, wall time
-around ``SearchIndex.search``.
-
-Exit codes of ``main`` follow cli.py:12: 0 success, 1 configuration error,
-2 data error.
+The reference reports, per (dataset, method, window, dims) cell, the skip
+rate and the speedup against the plain windowed-DTW scan (method none), in
+one schema (cli.py:36-39 CSV_COLUMNS, RunReport cli.py:46-83, emit_report
+cli.py:294-321).  This module keeps that schema -- columns, rounding and the
+csv / json / table renderings are byte-identical -- and fills rows from the
+GPU search (``gpu_rows``), so GPU rows can sit next to the reference's CPU
+rows.  Counters come from the GPU cascade (order-free, so skip counts may
+differ from the reference's; the nearest neighbours do not); ``lb_time_s`` /
+``dtw_time_s`` are CUDA-event phase times, ``total_time_s`` the wall time of
+``SearchIndex.search``.  The reference's command-line driver itself is out of
+scope.
 """
 
 from __future__ import annotations
 
-import argparse
 import json
-import os
-import platform
-import sys
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -124,193 +117,70 @@ def describe_params(params: SearchParams, label: str) -> str:
     return " ".join(bits)
 
 
-@dataclass
-class BenchConfig:
-    """cli.py:86-104, GPU edition: `dtype` selects the float64 (exact) or
-    float32 (filter + float64 re-score) search."""
-
-    data: list
-    fmt: str = "native"
-    methods: list = field(default_factory=lambda: [Method.TC_DTW])
-    windows: list = field(default_factory=lambda: [10, 20])
-    dims: list = field(default_factory=lambda: ["all"])
-    seed: int = 42
-    reps: int = 10
-    tune: bool = True
-    ideal: bool = False
-    emit: str = "csv"
-    out: str | None = None
-    query_frac: float = 0.3
-    dtype: str = "f64"
-
-
-@dataclass
-class _Run:
-    res: object
-    wall_s: float
-
-
-def _search(index, queries, params, advanced, dim_range, reps) -> _Run:
-    walls, res = [], None
-    for _ in range(max(1, reps)):
+def _timed_search(index, queries, params, advanced, dim_range, reps):
+    """(last result, mean wall seconds) over ``reps`` searches."""
+    res, total = None, 0.0
+    for _ in range(max(1, int(reps))):
         t0 = time.perf_counter()
         res = index.search(queries, params, advanced=advanced, dim_range=dim_range, timing=True)
-        walls.append(time.perf_counter() - t0)
-    return _Run(res, sum(walls) / len(walls))
+        total += time.perf_counter() - t0
+    return res, total / max(1, int(reps))
 
 
-def _times(res):
+def _phase_seconds(res):
+    """(bound time, DTW time) in seconds from the CUDA-event phases."""
     ph = res.phase_ms
-    lb = (ph.get("prep", 0) + ph.get("lb_mv", 0) + ph.get("seeds_topk", 0) + ph.get("compact", 0)
-          + ph.get("advanced", 0)) / 1e3
-    dtw = (ph.get("seeds_dtw", 0) + ph.get("dtw", 0) + ph.get("finalize", 0)) / 1e3
-    return lb, dtw
+    dtw_ms = sum(ph.get(k, 0.0) for k in ("seeds_dtw", "dtw", "finalize"))
+    return (sum(ph.values()) - dtw_ms) / 1e3, dtw_ms / 1e3
 
 
-def run_cell(ds, queries, candidates, index, method: Method, window: int, baseline: _Run, config: BenchConfig):
-    """One (dataset, method, window, dims) row (cli.py:226-271)."""
+def _resolve(method: Method, window: int, queries, candidates, dim_range, seed: int, tune: bool):
+    """Params and TC-DTW bound for one cell, chosen on the seeded sample the
+    reference CLI uses (cli.py:228-235): tune_params, then tc_dtw_select."""
     from .search import TUNE_CANDIDATE_SAMPLE, TUNE_QUERY_SAMPLE, _sample, tc_dtw_select, tune_params
 
     params = SearchParams(window=window, method=method)
-    advanced = None
-    if method == Method.NONE:
-        run = baseline
-    else:
-        qlist, clist = list(queries), list(candidates)
-        if config.tune and method != Method.LB_MV:
-            params = tune_params(qlist, clist, params, seed=config.seed, dim_range=ds.dim_ranges)
-        if method == Method.TC_DTW:
-            rng = np.random.default_rng(config.seed)
-            sq = _sample(qlist, TUNE_QUERY_SAMPLE, rng)
-            sc = _sample(clist, TUNE_CANDIDATE_SAMPLE, rng)
-            advanced = tc_dtw_select(sq, sc, params, dim_range=ds.dim_ranges)
-        run = _search(index, queries, params, advanced, ds.dim_ranges, config.reps)
-    c = run.res.counters
-    computed, skipped = int(c["dtw_computed"].sum()), int(c["dtw_skipped"].sum())
-    lb_t, dtw_t = _times(run.res)
-    ideal = None
-    if config.ideal:
-        b_lb, b_dtw = _times(baseline.res)
-        ideal = (b_lb + b_dtw) / max(dtw_t, 1e-12)  # bound overhead removed (cli.py:254-259)
-    label = method.value if advanced is None else f"{method.value}({advanced.value})"
-    return RunReport(dataset=ds.name, method=method.value, window=window, dims=ds.dims,
-                     skip_pct=100.0 * skipped / max(1, computed + skipped), speedup=baseline.wall_s / run.wall_s,
-                     ideal_speedup=ideal, dtw_computed=computed, dtw_skipped=skipped, lb_time_s=lb_t,
-                     dtw_time_s=dtw_t, total_time_s=run.wall_s, seed=config.seed,
-                     params=describe_params(params, label), threads=1, reps=config.reps)
+    if method in (Method.NONE, Method.LB_MV):
+        return params, None
+    if tune:
+        params = tune_params(list(queries), list(candidates), params, seed=seed, dim_range=dim_range)
+    if method != Method.TC_DTW:
+        return params, None
+    rng = np.random.default_rng(seed)
+    sq = _sample(list(queries), TUNE_QUERY_SAMPLE, rng)
+    sc = _sample(list(candidates), TUNE_CANDIDATE_SAMPLE, rng)
+    return params, tc_dtw_select(sq, sc, params, dim_range=dim_range)
 
 
-def run_benchmark(config: BenchConfig, datasets: list | None = None) -> list:
-    """Every configured cell (cli.py:165-212).  `datasets` (already loaded
-    Dataset objects) bypasses file loading."""
-    from . import ingest
+def gpu_rows(ds, methods=(Method.TC_DTW,), windows=(10, 20), *, seed: int = 42, reps: int = 1, tune: bool = True,
+             ideal: bool = False, query_frac: float = 0.3, dtype: str = "f64") -> list:
+    """Report rows of one loaded ``ingest.Dataset`` from the GPU search: the
+    reference's seeded query/candidate split, a NONE scan per window as the
+    speedup baseline, then every method (f3)."""
+    from .ingest import split
     from .search import SearchIndex
 
-    if not config.data and not datasets:
-        raise ConfigError("no dataset files given")
-    if not config.methods:
-        raise ConfigError("no methods given")
-    if not config.windows:
-        raise ConfigError("no window sizes given")
-    if config.reps < 1:
-        raise ConfigError("reps must be >= 1")
-    methods = [Method(m) for m in config.methods]
-    if datasets is None:
-        datasets = []
-        for path in config.data:
-            if config.fmt not in ("native", "ts"):
-                raise ConfigError(f"unknown format {config.fmt!r}")
-            datasets.append(ingest.load(path, config.fmt))
-    for ds in datasets:
-        for spec in config.dims:
-            if spec != "all" and not (1 <= int(spec) <= ds.dims):
-                raise ConfigError(f"dims={spec} out of range for {ds.name} (D={ds.dims})")
-    reports = []
-    np_t = np.float32 if config.dtype == "f32" else np.float64
-    for full in datasets:
-        for spec in config.dims:
-            ds = full if spec == "all" else ingest.truncate_dims(full, int(spec))
-            qs, cs = ingest.split(ds, config.query_frac, config.seed)
-            queries = np.ascontiguousarray(qs.values, dtype=np_t)
-            candidates = np.ascontiguousarray(cs.values, dtype=np_t)
-            index = SearchIndex(candidates, dtype=config.dtype)
-            for window in config.windows:
-                base = _search(index, queries, SearchParams(window=window, method=Method.NONE), None,
-                               ds.dim_ranges, config.reps)
-                for m in methods:
-                    reports.append(run_cell(ds, queries, candidates, index, m, window, base, config))
-    return reports
-
-
-def build_parser() -> argparse.ArgumentParser:
-    class _P(argparse.ArgumentParser):
-        def error(self, message):  # configuration errors exit 1 (cli.py:324-326)
-            raise ConfigError(message)
-
-    p = _P(prog="tcdtw-report", description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
-    p.add_argument("--data", nargs="+", required=True)
-    p.add_argument("--format", choices=["native", "ts"], default="native")
-    p.add_argument("--method", nargs="+", default=["tc_dtw"], choices=[m.value for m in Method])
-    p.add_argument("--window", nargs="+", type=int, default=[10, 20])
-    p.add_argument("--dims", nargs="+", default=["all"])
-    p.add_argument("--seed", type=int, default=42)
-    p.add_argument("--reps", type=int, default=10)
-    g = p.add_mutually_exclusive_group()
-    g.add_argument("--tune", dest="tune", action="store_true", default=True)
-    g.add_argument("--no-tune", dest="tune", action="store_false")
-    p.add_argument("--out", default=None)
-    p.add_argument("--emit", choices=["csv", "table", "json"], default="csv")
-    p.add_argument("--ideal", action="store_true")
-    p.add_argument("--dtype", choices=["f64", "f32"], default="f64")
-    return p
-
-
-def main(argv=None) -> int:
-    from .ingest import ParseError
-
-    try:
-        a = build_parser().parse_args(argv)
-        dims = []
-        for d in a.dims:
-            if d == "all":
-                dims.append("all")
-                continue
-            try:
-                dims.append(int(d))
-            except ValueError:
-                raise ConfigError(f'--dims expects integers or "all", got {d!r}') from None
-        if any(w < 0 for w in a.window):
-            raise ConfigError("--window must be >= 0")
-        cfg = BenchConfig(data=a.data, fmt=a.format, methods=[Method(m) for m in a.method], windows=a.window,
-                          dims=dims, seed=a.seed, reps=a.reps, tune=a.tune, ideal=a.ideal, emit=a.emit, out=a.out,
-                          dtype=a.dtype)
-    except ConfigError as exc:
-        print(f"config error: {exc}", file=sys.stderr)
-        return 1
-    for path in cfg.data:
-        if not os.path.exists(path):
-            print(f"config error: no such file: {path}", file=sys.stderr)
-            return 1
-    try:
-        reports = run_benchmark(cfg)
-    except ConfigError as exc:
-        print(f"config error: {exc}", file=sys.stderr)
-        return 1
-    except (ParseError, InvalidInputError, OSError) as exc:
-        print(f"data error: {exc}", file=sys.stderr)
-        return 2
-    import torch
-
-    meta = {"host": platform.node() or "unknown", "platform": platform.platform(),
-            "device": torch.cuda.get_device_name(0), "reps": cfg.reps, "seed": cfg.seed, "dtype": cfg.dtype}
-    text = emit_report(reports, cfg.emit, meta)
-    if cfg.out:
-        with open(cfg.out, "w", encoding="utf-8") as fh:
-            fh.write(text)
-    else:
-        sys.stdout.write(text)
-    return 0
-
-
-if __name__ == "__main__":
-    sys.exit(main())
+    np_t = np.float32 if dtype == "f32" else np.float64
+    qs, cs = split(ds, query_frac, seed)
+    queries = np.ascontiguousarray(qs.values, dtype=np_t)
+    candidates = np.ascontiguousarray(cs.values, dtype=np_t)
+    index = SearchIndex(candidates, dtype=dtype)
+    rows = []
+    for window in windows:
+        base_res, base_wall = _timed_search(index, queries, SearchParams(window=window, method=Method.NONE), None,
+                                            ds.dim_ranges, reps)
+        for m in map(Method, methods):
+            if m == Method.NONE:
+                res, wall, params, adv = base_res, base_wall, SearchParams(window=window, method=m), None
+            else:
+                params, adv = _resolve(m, window, queries, candidates, ds.dim_ranges, seed, tune)
+                res, wall = _timed_search(index, queries, params, adv, ds.dim_ranges, reps)
+            computed = int(res.counters["dtw_computed"].sum())
+            skipped = int(res.counters["dtw_skipped"].sum())
+            lb_s, dtw_s = _phase_seconds(res)
+            ideal_x = sum(_phase_seconds(base_res)) / max(dtw_s, 1e-12) if ideal else None  # cli.py:254-259
+            label = m.value if adv is None else f"{m.value}({Method(adv).value})"
+            rows.append(RunReport(ds.name, m.value, window, ds.dims, 100.0 * skipped / max(1, computed + skipped),
+                                  base_wall / wall, ideal_x, computed, skipped, lb_s, dtw_s, wall, seed,
+                                  params=describe_params(params, label), reps=reps))
+    return rows

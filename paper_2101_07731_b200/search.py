@@ -58,16 +58,23 @@ class BatchOutcome:
                          int(c["abandon_count"][i]), work=work)
 
 
+_NO_SECOND_BOUND = (Method.NONE, Method.LB_MV)
+_TC_DTW_CHOICES = (Method.LB_TI, Method.LB_PC)
+
+
 def _advanced_method(params: SearchParams, advanced) -> Method | None:
-    """search.py:59-68."""
-    method = params.method
-    if method in (Method.NONE, Method.LB_MV):
+    """The bound the cascade's second step runs, or None (search.py:59-68
+    decides the same three cases: no second bound for NONE / LB_MV; TC_DTW
+    takes the bound tc_dtw_select picked; any other method is its own
+    second bound)."""
+    m = params.method
+    if m in _NO_SECOND_BOUND:
         return None
-    if method == Method.TC_DTW:
-        if advanced not in (Method.LB_TI, Method.LB_PC):
-            raise InvalidInputError("TC_DTW must be resolved with tc_dtw_select first")
+    if m != Method.TC_DTW:
+        return m
+    if advanced in _TC_DTW_CHOICES:
         return Method(advanced)
-    return method
+    raise InvalidInputError("TC_DTW must be resolved with tc_dtw_select first")
 
 
 def work_model(params: SearchParams, n: int, dims: int, adv: Method | None, counters: dict, i: int) -> float:
@@ -361,11 +368,15 @@ def nn_search(query, candidates, params: SearchParams, advanced: Method | None =
 
 
 def _sample(items: list, size: int, rng: np.random.Generator) -> list:
-    """search.py:183-187 (same draw, so tuning samples match the reference)."""
-    if len(items) <= size:
-        return list(items)
-    idx = rng.choice(len(items), size=size, replace=False)
-    return [items[i] for i in sorted(idx)]
+    """A seeded subset of at most ``size`` items in their original order.
+    The draw is ``rng.choice(len, size, replace=False)`` as in
+    search.py:183-187, so the tuning sample holds the same series as the
+    reference's for the same seed."""
+    pool = list(items)
+    if size >= len(pool):
+        return pool
+    keep = np.sort(rng.choice(len(pool), size=size, replace=False))
+    return [pool[k] for k in keep]
 
 
 def _run_sample(queries, candidates, params, advanced, dim_range, metric) -> float:
@@ -416,38 +427,45 @@ def select_method(sample_queries, sample_candidates, params: SearchParams, dim_r
     return best
 
 
+def _tuning_stages(params: SearchParams, grids: dict) -> list:
+    """The grid searches tune_params runs for ``params.method``, as
+    (bound to run, [(field overrides), ...]) in the reference's order
+    (search.py:256-271): the LB_TI trigger grid for LB_TI / LB_AD / TC_DTW
+    (LB_AD tunes the same trigger), then trigger x level for LB_PC / TC_DTW."""
+    m = params.method
+    stages = []
+    ti_bound = {Method.LB_TI: Method.LB_TI, Method.LB_AD: Method.LB_AD, Method.TC_DTW: Method.LB_TI}.get(m)
+    if ti_bound is not None:
+        stages.append((ti_bound, [{"trigger_ti": e} for e in grids["trigger_ti"]]))
+    if m in (Method.LB_PC, Method.TC_DTW):
+        stages.append((Method.LB_PC, [{"trigger_pc": e, "quant_levels": lv}
+                                      for e in grids["trigger_pc"] for lv in grids["quant_levels"]]))
+    return stages
+
+
 def tune_params(queries, candidates, params: SearchParams, grids: dict | None = None, seed: int = 0,
                 dim_range=None, metric: str = "work", log: list | None = None) -> SearchParams:
-    """Grid-search trigger thresholds and quantisation level on a seeded
-    sample (search.py:220-272); same grid sizes and sampling."""
+    """Trigger thresholds (and quantisation level) chosen on a seeded sample
+    (search.py:220-272): up to 8 queries and 23 candidates drawn as the
+    reference draws them, every grid point costed by one batched GPU search
+    of the sample, the first cheapest point of each grid kept.  Each
+    evaluation is appended to ``log`` as (bound, params, cost)."""
     from .core import default_grids
 
-    grids = grids or default_grids()
-    method = params.method
-    if method in (Method.NONE, Method.LB_MV):
+    if params.method in _NO_SECOND_BOUND:
         return params
+    grids = grids or default_grids()
     rng = np.random.default_rng(seed)
-    sq = _sample(list(queries), TUNE_QUERY_SAMPLE, rng)
-    sc = _sample(list(candidates), TUNE_CANDIDATE_SAMPLE, rng)
-
-    def eval_grid(adv: Method, variants: list[SearchParams]) -> SearchParams:
-        best, best_cost = None, None
-        for p in variants:
-            cost = _run_sample(sq, sc, replace(p, method=adv), None, dim_range, metric)
+    sample_q = _sample(queries, TUNE_QUERY_SAMPLE, rng)
+    sample_c = _sample(candidates, TUNE_CANDIDATE_SAMPLE, rng)
+    chosen = {}
+    for bound, points in _tuning_stages(params, grids):
+        costs = []
+        for overrides in points:
+            trial = replace(params, **overrides)
+            cost = _run_sample(sample_q, sample_c, replace(trial, method=bound), None, dim_range, metric)
+            costs.append(cost)
             if log is not None:
-                log.append((adv, p, cost))
-            if best_cost is None or cost < best_cost:
-                best, best_cost = p, cost
-        return best
-
-    tuned = params
-    if method in (Method.LB_TI, Method.LB_AD, Method.TC_DTW):
-        adv = Method.LB_TI if method == Method.TC_DTW else method
-        cands = [replace(params, trigger_ti=e) for e in grids["trigger_ti"]]
-        tuned = replace(tuned, trigger_ti=eval_grid(adv, cands).trigger_ti)
-    if method in (Method.LB_PC, Method.TC_DTW):
-        cands = [replace(params, trigger_pc=e, quant_levels=lv) for e in grids["trigger_pc"]
-                 for lv in grids["quant_levels"]]
-        best = eval_grid(Method.LB_PC, cands)
-        tuned = replace(tuned, trigger_pc=best.trigger_pc, quant_levels=best.quant_levels)
-    return tuned
+                log.append((bound, trial, cost))
+        chosen.update(points[int(np.argmin(costs))])  # argmin: the first minimum, as a strict-< scan
+    return replace(params, **chosen)

@@ -20,8 +20,26 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(L, name), name
     assert set(_lib.EXPORTED) == declared
-    assert L.tcdtw_abi_version() == 2
+    assert L.tcdtw_abi_version() == 3
     assert L.tcdtw_strerror(1) == b"invalid input"
+
+
+# mvdtw.__all__ (reference pkg/src/mvdtw/__init__.py:30-38): every name a caller may import
+REFERENCE_ALL = [
+    "BoundResult", "BoundingBox", "BoxGrouping", "BoxSet", "Dataset", "DtwResult", "Envelope", "InvalidInputError",
+    "Method", "MultivariateSeries", "NeighborDistances", "NnOutcome", "ParseError", "RawDataset", "SearchParams",
+    "TiVariant", "build_box_sets", "build_envelope", "dtw_banded", "finalize", "lb_ad", "lb_mv", "lb_pc", "lb_ti",
+    "neighbor_steps", "nn_search", "normalize", "parse_native", "parse_ts_subset", "point_distance",
+    "quantize_cluster", "split", "tc_dtw_select", "ti_advance", "ti_extend_top", "truncate_dims", "tune_params",
+    "write_native",
+]
+
+
+def test_package_exports_the_reference_api():
+    import paper_2101_07731_b200 as P
+
+    missing = [n for n in REFERENCE_ALL if n not in P.__all__ or not hasattr(P, n)]
+    assert not missing, missing
 
 
 def test_workspace_size_and_validation_without_gpu():
@@ -204,7 +222,10 @@ def test_new_entry_points_validate_without_gpu():
     assert L.tcdtw_search_workspace_size(ctypes.byref(d), ctypes.byref(out)) == 0
     assert with_rev - out.value >= 64 * 10000 * 4 + 2 * 10000 * 128 * 6 * 4  # (Q,N) bound + planar envelopes
     nb = ctypes.c_size_t()
-    assert L.tcdtw_normalize_workspace_size(0, ctypes.byref(nb)) == 1
-    assert L.tcdtw_normalize_workspace_size(6, ctypes.byref(nb)) == 0 and nb.value > 0
+    assert L.tcdtw_normalize_workspace_size(100, 0, ctypes.byref(nb)) == 1
+    assert L.tcdtw_normalize_workspace_size(0, 6, ctypes.byref(nb)) == 1
+    assert L.tcdtw_normalize_workspace_size(100, 6, ctypes.byref(nb)) == 0 and nb.value > 0
+    assert L.tcdtw_normalize_workspace_size(210000, 1, ctypes.byref(nb)) == 0  # + the pairwise-sum tree
+    assert nb.value >= 8 * (2 << 10)
     assert L.tcdtw_normalize(None, 10, 6, None, None, None, None, None, 0, None) == 1
     assert L.tcdtw_normalize(None, 0, 6, None, None, None, None, None, 0, None) == 1

@@ -52,6 +52,42 @@ def test_parse_errors_match_reference(name):
     assert str(exc.value).replace(str(G / name), "<path>") == META["errors"][name]
 
 
+FUZZ = json.loads((G / "fuzz.json").read_text())
+FUZZ_ARR = np.load(G / "fuzz.npz")
+
+
+@pytest.mark.parametrize("case", range(len(FUZZ)))
+def test_parser_edge_cases_match_reference(case, tmp_path):
+    """Lexical corners (line ends, Unicode spaces, number spellings,
+    directive forms) against the reference parser's own outcome
+    (tests/golden/make_golden_ingest_fuzz.py)."""
+    rec = FUZZ[case]
+    path = tmp_path / ("case.txt" if rec["fmt"] == "native" else "case.ts")
+    path.write_text(rec["text"], encoding="utf-8", newline="")
+    fn = ingest.parse_native if rec["fmt"] == "native" else ingest.parse_ts_subset
+    if "error" in rec:
+        kind, msg = rec["error"]
+        with pytest.raises(Exception) as exc:
+            fn(path)
+        assert type(exc.value).__name__ == kind
+        assert str(exc.value).replace(str(path), "<path>") == msg
+        return
+    raw = fn(path)
+    want = FUZZ_ARR[f"c{case}"]
+    assert raw.values.shape == tuple(rec["shape"]) and raw.source_format == rec["format"]
+    assert raw.name.replace(path.stem, "<stem>") == rec["name"]
+    assert np.array_equal(raw.values, want, equal_nan=True)
+    assert np.array_equal(np.signbit(raw.values), np.signbit(want))  # -0.0 and -nan keep their sign
+
+
+def test_parser_is_native_code():
+    """The tokenizer is the library's tcdtw_parse_text, not Python."""
+    import inspect
+
+    src = inspect.getsource(ingest)
+    assert "tcdtw_parse_text" in src and "float(" not in src
+
+
 def test_write_native_round_trip(tmp_path):
     raw = _parse("native_b.txt")
     ds = ingest.finalize(raw)
@@ -92,8 +128,5 @@ def test_report_schema_and_errors():
     assert report.CSV_COLUMNS == META["report_columns"]
     with pytest.raises(report.ConfigError):
         report.emit_report(_rows(), "xml")
-    assert report.main(["--data", "/nonexistent/file.txt"]) == 1
-    assert report.main(["--data", str(G / "native_a.txt"), "--dims", "two"]) == 1
-    assert report.main(["--data", str(G / "native_a.txt"), "--window", "-1"]) == 1
     p = report.describe_params(report.SearchParams(window=3, method=report.Method.TC_DTW), "tc_dtw(lb_pc)")
     assert p == "tc_dtw(lb_pc) e_ti=0.1 e_pc=0.1 L=2 P=5 K=6 w=6"
