@@ -66,56 +66,79 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    (nvidia-ml-py) polled every 5 ms from a thread, plus one sample at entry
+    and exit, so even millisecond-long regions get samples; nvidia-smi
+    (-lms 100) if NVML is unavailable."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_s: float = 0.005):
         self.gpu = gpu_index
-        self.proc = None
-        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"tcdtw_clocks_{os.getpid()}.csv"
+        self.period = period_s
+        self.rows = []  # (sm_mhz, max_mhz, reason bits)
+        self._stop = None
+        self._thread = None
+        self._nvml = None
+        self._h = None
+
+    def _sample(self):
+        n = self._nvml
+        reasons = getattr(n, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            n.nvmlDeviceGetCurrentClocksThrottleReasons
+        self.rows.append((n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM),
+                          n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM), int(reasons(self._h))))
+
+    def _loop(self):
+        while not self._stop.wait(self.period):
+            try:
+                self._sample()
+            except Exception:
+                return
 
     def __enter__(self):
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self._physical_index())
+            self._sample()
         except Exception:
-            self.proc = None
+            self._nvml = None
+            return self
+        self._stop = threading.Event()
+        self._thread = threading.Thread(target=self._loop, daemon=True)
+        self._thread.start()
         return self
 
+    def _physical_index(self) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [v.strip() for v in vis.split(",") if v.strip()]
+            if self.gpu < len(ids) and ids[self.gpu].isdigit():
+                return int(ids[self.gpu])
+        return self.gpu
+
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=2)
+        if self._nvml is not None:
             try:
-                self.proc.wait(timeout=5)
+                self._sample()
             except Exception:
-                self.proc.kill()
+                pass
 
     def summary(self):
-        try:
-            rows = [r.split(",") for r in self.path.read_text().strip().splitlines() if r.strip()]
-        except Exception:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in rows:
-            for k, nm in enumerate(names):
-                if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
-                    reasons.add(nm)
-        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-               "reasons": sorted(reasons), "samples": len(rows)}
-        try:
-            self.path.unlink()
-        except Exception:
-            pass
-        return out
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        reasons = sorted(nm for nm, bit in self.REASONS.items() if any(r[2] & bit for r in self.rows))
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
 
 
 def traffic_from_profile(cells_per_launch=None):
@@ -391,7 +414,8 @@ def run_ours(args):
     # ALU issue-rate probe (FP32 FFMA, independent chains) on this box
     lane_ops = __import__("ctypes").c_double()
     # the DTW arithmetic type's FMA rate (FP64 issues at half the FP32 rate)
-    probe_dt = 1 if wl.dtype == "f64" else 0
+    dtw_f32 = wl.dtype == "f32" or index.f32_filter  # float64 data under the float32 filter
+    probe_dt = 0 if dtw_f32 else 1
     sink = torch.empty(1, device="cuda", dtype=torch.float64)
     L.tcdtw_alu_probe(probe_dt, 148 * 8, 2000, sink.data_ptr(), __import__("ctypes").byref(lane_ops),
                       _lib.stream_ptr())
@@ -425,10 +449,14 @@ def run_ours(args):
         roof = {"kernel": index.dtw_kernel(params, advanced, batch), "bound": "alu", "achieved": achieved, "peak": alu_peak,
                 "unit": "Tlane-op/s", "frac": achieved / alu_peak, "traffic": traffic_from_profile(dtw_cells / max(1, -(-n_q // batch))),
                 "algorithmic_ops": f"(2d+4) = {2 * d + 4} per DP cell x {dtw_cells:.4g} cells (SURVEY 8d)"}
-    lanes = 64 if wl.dtype == "f64" else 128
-    roof["peak_source"] = (f"tcdtw_alu_probe {'DFMA' if wl.dtype == 'f64' else 'FFMA'} issue rate measured in this "
+    lanes = 128 if dtw_f32 else 64
+    nominal = 148 * lanes * measured_peaks().get("sm_max_mhz", 1965) / 1e6
+    roof["peak_source"] = (f"tcdtw_alu_probe {'FFMA' if dtw_f32 else 'DFMA'} issue rate measured in this "
                            f"run (nominal 148 SM x {lanes} lanes x {measured_peaks().get('sm_max_mhz', 1965)} MHz = "
-                           f"{148 * lanes * measured_peaks().get('sm_max_mhz', 1965) / 1e6:.1f} T)")
+                           f"{nominal:.1f} T)")
+    roof["frac_of_nominal"] = roof["achieved"] / nominal
+    roof["arithmetic"] = ("float32 filter on float64 inputs + float64 finalist re-score" if index.f32_filter
+                          else ("float32 filter + float64 finalist re-score" if wl.dtype == "f32" else "float64"))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -159,10 +159,24 @@ typedef struct tcdtw_search_desc {
      * forward terms. */
     const void *cand_upper;
     const void *cand_lower;
+    /* Capacity of the completed-DTW list the finalisation visits (0 =
+     * default); when it overflows, every survivor tile is scanned instead.
+     * Tests set 1 to exercise that path (ABI version 3). */
+    int64_t done_cap;
 } tcdtw_search_desc;
 
 #define TCDTW_FLAG_TIMING 1     /* fill desc->phase_ms (synchronises the stream) */
 #define TCDTW_FLAG_REVERSE_LB 2 /* also prune on the candidate-envelope bound */
+/* dtype must be TCDTW_F64.  The filter (bounds, seeds, DTW with abandoning)
+ * runs in float32 on float32 roundings of the inputs, made in the workspace
+ * by the seed phase; decisions carry an extra absolute slack that covers the
+ * rounding (2.5 (2n-1) 2^-24 (max|q| + max|c|)), and the finalists are
+ * re-scored in float64 on the original inputs, so best_distance is the
+ * reference's float64 value and best_index its lowest-index argmin.  d_best
+ * is then float32.  Inputs must lie inside the float32 range.  Not combined
+ * with TCDTW_FLAG_REVERSE_LB. */
+#define TCDTW_FLAG_F32_FILTER 4
+#define TCDTW_FLAG_DEBUG_SYNC 8 /* synchronise + report to stderr after every stage */
 #define TCDTW_PHASES 8      /* prep, lb_mv, seeds_topk, seeds_dtw, compact, advanced, dtw, finalize */
 #define TCDTW_COUNTERS 9    /* per query: see enum below */
 
@@ -190,7 +204,11 @@ int tcdtw_search_seed(const tcdtw_search_desc *desc, const void *queries, const 
 
 /* Phase 2: survivor compaction against d_best, the advanced bound on the
  * trigger band, DTW with early abandoning, lexicographic (distance, index)
- * reduction with float64 finalist re-scoring.  best_index is global
+ * reduction with float64 finalist re-scoring.  Purely asynchronous: the
+ * survivor and tile counts stay on the device (the grids are sized by their
+ * upper bounds), so the host never waits -- a sharded caller's d_best
+ * exchange of batch k overlaps the GPU work of batch k+1 (only
+ * TCDTW_FLAG_TIMING / TCDTW_FLAG_DEBUG_SYNC synchronise).  best_index is global
  * (candidate_base added; -1 if every candidate of this shard was pruned
  * against a better d_best from another shard, with best_distance +inf).
  * counters: (n_queries, TCDTW_COUNTERS) int64. */

@@ -24,6 +24,8 @@ COUNTERS = ("dtw_computed", "dtw_skipped", "lb_mv_evals", "advanced_lb_evals", "
             "dtw_cells", "finalists", "survivors", "cells_issued")
 FLAG_TIMING = 1
 FLAG_REVERSE_LB = 2
+FLAG_F32_FILTER = 4
+FLAG_DEBUG_SYNC = 8
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -44,6 +46,7 @@ class SearchDesc(ctypes.Structure):
         ("min_cell_frac", ctypes.c_double), ("n_queries", _i64), ("n_candidates", _i64),
         ("candidate_base", _i64), ("seeds", _i32), ("flags", _i32),
         ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("cand_upper", _vp), ("cand_lower", _vp),
+        ("done_cap", _i64),
     ]
 
 

@@ -41,7 +41,6 @@ inline std::atomic<unsigned long long> g_launches{0};
 inline int launch_status() {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess && getenv("TCDTW_DEBUG")) fprintf(stderr, "[tcdtw] CUDA error: %s\n", cudaGetErrorString(e));
     return e == cudaSuccess ? TCDTW_OK : TCDTW_CUDA_ERROR;
 }
 

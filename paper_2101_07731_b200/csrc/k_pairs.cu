@@ -731,11 +731,10 @@ int series_envelope(int dtype, const void* s, int64_t ns, int n, int d, int w, v
     const int64_t total = ns * (int64_t)n * d;
     const size_t es = dtype == TCDTW_F64 ? 8 : 4;
     const size_t per_series = (size_t)6 * n * d * es;  // 2 staging + 4 scan arrays
-    static const bool naive = getenv("TCDTW_ENV_NAIVE") != nullptr;  // A/B switch
-    if (!naive && per_series + (size_t)8 * n <= 200 * 1024 && n < (1 << 30)) {
+    if (per_series + (size_t)8 * n <= 200 * 1024 && n < (1 << 30)) {
         // ~72 KB per block (3 resident per SM): each keeps one group of
         // reads in flight while it scans the previous one
-        static const int kb = getenv("TCDTW_ENV_KB") ? atoi(getenv("TCDTW_ENV_KB")) : 54;  // A/B: staging KB (54: best of 18-72)
+        constexpr int kb = 54;  // staging KB per block (18 / 36 / 54 / 72 KB measured: 54 best)
         int G = (int)((kb * 1024) / per_series);
         G = G < 1 ? 1 : G;
         const size_t smem = per_series * G + (size_t)8 * n;  // + the per-row window table

@@ -60,27 +60,22 @@ int lb_mv_matrix(int dtype, const void* up, const void* lo, const void* cands, i
 const char* dtw_kernel_name(const tcdtw_search_desc* dsc) {
     Plan p;
     if (make_plan(dsc, &p) != TCDTW_OK) return "invalid";
-    if (getenv("TCDTW_NO_LANE") == nullptr) {
-        if (!p.exact) {
-            const int r = laner_rows_shape(p.n, p.d, p.B);
-            if (r == 4) return "dtw_laner_kernel<R=4>";
-            if (r == 2) return "dtw_laner_kernel<R=2>";
-        }
-        bool lane = false;
+    if (!p.exact) {
+        const int r = laner_rows_shape(p.n, p.d, p.B);
+        if (r == 4) return "dtw_laner_kernel<R=4>";
+        if (r == 2) return "dtw_laner_kernel<R=2>";
+    }
+    bool lane = false;
 #define TCDTW_NAME_CASE(TT, DD, BB) lane = lane || ((sizeof(TT) == 8) == p.exact && p.d == DD && p.B == BB);
-        TCDTW_LANE_SPECS(TCDTW_NAME_CASE)
+    TCDTW_LANE_SPECS(TCDTW_NAME_CASE)
 #undef TCDTW_NAME_CASE
-        if (lane) return "dtw_lane_kernel";
-    }
+    if (lane) return "dtw_lane_kernel";
     if (p.B <= 64) return "dtw_tpp_kernel";
-    if (getenv("TCDTW_PIPE") && p.w >= 32) return "dtw_pipe_kernel";
-    if (!getenv("TCDTW_WAVE_GENERIC")) {
-        bool wd = false;
+    bool wd = false;
 #define TCDTW_WAVE_NAME(DD) wd = wd || p.d == DD;
-        TCDTW_WAVE_DIMS(TCDTW_WAVE_NAME)
+    TCDTW_WAVE_DIMS(TCDTW_WAVE_NAME)
 #undef TCDTW_WAVE_NAME
-        if (wd) return "dtw_wave_d_kernel";
-    }
+    if (wd) return "dtw_wave_d_kernel";
     return "dtw_wave_kernel";
 }
 

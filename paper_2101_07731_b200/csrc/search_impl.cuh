@@ -74,20 +74,31 @@ __host__ __device__ inline int64_t cells_upto(int r, int n, int w) {
     return (R + 1) + s1 + s2 - s3;
 }
 
+// Float32 decisions carry an affine margin: threshold = value * mult + add.
+// `mult` covers float32 arithmetic on the inputs as given; `add` (device
+// pointer, nullptr = 0) covers the rounding of float64 inputs to float32
+// when the float32 filter runs on float64 data (TCDTW_FLAG_F32_FILTER):
+// add[0] for prune / abandon thresholds, add[1] for finalists.
 struct Margins {
     float prune;  // d_best multiplier for prune / abandon thresholds
     float fin;    // best multiplier for finalists
+    const float* add;
 };
 
 template <typename T>
-__device__ __forceinline__ T scale_up(T v, float m);
+__device__ __forceinline__ T scale_up(T v, const Margins& mg);
 template <>
-__device__ __forceinline__ float scale_up<float>(float v, float m) {
-    return __fmul_ru(v, m);
+__device__ __forceinline__ float scale_up<float>(float v, const Margins& mg) {
+    const float t = __fmul_ru(v, mg.prune);
+    return mg.add ? __fadd_ru(t, __ldg(mg.add)) : t;
 }
 template <>
-__device__ __forceinline__ double scale_up<double>(double v, float) {
+__device__ __forceinline__ double scale_up<double>(double v, const Margins&) {
     return v;  // EXACT: no margin
+}
+__device__ __forceinline__ float fin_up(float v, const Margins& mg) {
+    const float t = __fmul_ru(v, mg.fin);
+    return mg.add ? __fadd_ru(t, __ldg(mg.add + 1)) : t;
 }
 
 // ------------------------------------------------------- planar transpose
@@ -495,7 +506,30 @@ struct Tiles {
     uint32_t* q;      // query of the tile
     int64_t* begin;   // first entry
     int32_t* len;     // entries (<= 32)
+    // number of tiles on the device (written by the compaction's scan), so
+    // the host never waits for it; nullptr: the kernels' n_tiles argument
+    const int64_t* count = nullptr;
 };
+
+// Tiles a kernel works through: the device count when there is one (the
+// host passes an upper bound for grid sizing), else the argument.
+__device__ __forceinline__ int64_t tile_count(const Tiles& t, int64_t n_tiles) {
+    return t.count ? *t.count : n_tiles;
+}
+
+// Survivor piece length of the R-row lane kernel, from the device tile
+// count: whole 2048-entry segments when there are at least 4 per resident
+// warp, else pieces of about survivors / (4 x warps), at least 128.
+static __global__ void laner_seglen_kernel(const int64_t* __restrict__ tiles32, int64_t warps, int* __restrict__ out) {
+    const int64_t surv_est = *tiles32 * (int64_t)kTile;
+    int seg_len = (int)kChunk;
+    if (surv_est / kChunk < 4 * warps) {
+        const int64_t want = surv_est / (4 * warps);
+        seg_len = 128;
+        while (seg_len < want && seg_len < (int)kChunk) seg_len <<= 1;
+    }
+    *out = seg_len;
+}
 
 // seed list: one tile per query (S <= 32 entries at q*S)
 static __global__ void seed_tiles_kernel(int64_t Q, int S, const int32_t* __restrict__ seed_cnt, Tiles t) {
@@ -532,7 +566,7 @@ __global__ void __launch_bounds__(256) compact_count_kernel(const T* __restrict_
     const int ns = S > 0 ? seed_cnt[q] : 0;
     if (threadIdx.x < ns) sd[threadIdx.x] = seeds[q * S + threadIdx.x];
     __syncthreads();
-    const T thr = all ? T(0) : scale_up<T>(dbest[q], mg.prune);
+    const T thr = all ? T(0) : scale_up<T>(dbest[q], mg);
     const T* row = lb ? lb + q * N : nullptr;
     const T* row2 = lb2 ? lb2 + q * N : nullptr;
     const int64_t c0 = (int64_t)chunk * kChunk;
@@ -566,7 +600,7 @@ __global__ void __launch_bounds__(256) compact_write_kernel(const T* __restrict_
     if (threadIdx.x < ns) sd[threadIdx.x] = seeds[q * S + threadIdx.x];
     if (threadIdx.x == 0) base_s = chunk_off[(int64_t)chunk * gridDim.y + q];
     __syncthreads();
-    const T thr = all ? T(0) : scale_up<T>(dbest[q], mg.prune);
+    const T thr = all ? T(0) : scale_up<T>(dbest[q], mg);
     const T* row = lb ? lb + q * N : nullptr;
     const T* row2 = lb2 ? lb2 + q * N : nullptr;
     const int64_t c0 = (int64_t)chunk * kChunk;
@@ -613,8 +647,9 @@ __global__ void poison_seeds_kernel(T* __restrict__ lb, int64_t N, int64_t Q, in
 // per-(chunk, query) survivor segments -> tile counts; then fill
 static __global__ void seg_tiles_count_kernel(int64_t Q, int n_chunks, const int64_t* __restrict__ chunk_off,
                                        int64_t* __restrict__ tile_cnt, int64_t* __restrict__ counters,
-                                       int tile_len = kTile) {
+                                       int tile_len = kTile, const int* __restrict__ tile_len_dev = nullptr) {
     const int64_t n_seg = Q * n_chunks;
+    if (tile_len_dev) tile_len = *tile_len_dev;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_seg; g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t cnt = chunk_off[g + 1] - chunk_off[g];
         tile_cnt[g] = (cnt + tile_len - 1) / tile_len;
@@ -624,8 +659,10 @@ static __global__ void seg_tiles_count_kernel(int64_t Q, int n_chunks, const int
 }
 
 static __global__ void seg_tiles_fill_kernel(int64_t Q, int n_chunks, const int64_t* __restrict__ chunk_off,
-                                      const int64_t* __restrict__ tile_off, Tiles t, int tile_len = kTile) {
+                                      const int64_t* __restrict__ tile_off, Tiles t, int tile_len = kTile,
+                                      const int* __restrict__ tile_len_dev = nullptr) {
     const int64_t n_seg = Q * n_chunks;
+    if (tile_len_dev) tile_len = *tile_len_dev;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_seg; g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = chunk_off[g], e = chunk_off[g + 1];
         const int64_t t0 = tile_off[g];
@@ -670,6 +707,10 @@ struct SArgs {
     // W + 8 after, (Q, qpad_rows, (d+1)/2) float2, staged by the R-row lane kernel
     const float2* qpad;
     int qpad_rows;
+    // TCDTW_FLAG_F32_FILTER: the float64 inputs the finalists are re-scored
+    // on (queries / cands are then their float32 roundings); else nullptr
+    const double* xq;
+    const double* xc;
 };
 
 template <typename T>
@@ -697,6 +738,7 @@ template <typename T, int DMAX, int BMAX, bool EXACT>
 __global__ void __launch_bounds__(256) dtw_tpp_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
                                                       const uint32_t* __restrict__ cand_of, T* __restrict__ res,
                                                       int* __restrict__ tile_ctr) {
+    n_tiles = tile_count(tl, n_tiles);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int VEC = 16 / sizeof(T);
     const int n = a.n, d = a.d, w = a.w, B = 2 * w + 1;
@@ -735,7 +777,7 @@ __global__ void __launch_bounds__(256) dtw_tpp_kernel(SArgs<T> a, Tiles tl, int6
         T band[BMAX];
 #pragma unroll
         for (int k = 0; k < BMAX; ++k) band[k] = (k == w) ? T(0) : INF;
-        T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg.prune) : INF;
+        T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg) : INF;
         bool done = !active;
         int stop_row = n - 1;
         bool abandoned = false;
@@ -810,7 +852,7 @@ __global__ void __launch_bounds__(256) dtw_tpp_kernel(SArgs<T> a, Tiles tl, int6
                 stop_row = i;
             }
             if (__all_sync(0xffffffffu, done)) break;
-            if ((i & 7) == 7 && a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg.prune);
+            if ((i & 7) == 7 && a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg);
 #pragma unroll
             for (int p = 0; p < DMAX; ++p) cpt[p] = cnext[p];
         }
@@ -991,6 +1033,7 @@ template <typename T, int D, int B, bool EXACT, bool VEC>
 __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
                                                       const uint32_t* __restrict__ cand_of, T* __restrict__ res,
                                                       int* __restrict__ tile_ctr) {
+    n_tiles = tile_count(tl, n_tiles);
     constexpr int W = (B - 1) / 2;
     constexpr int DP = (D + 1) / 2;     // coordinate pairs per point
     constexpr bool QV = (D % 2 == 0);   // query/envelope rows as pairs
@@ -1177,7 +1220,7 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
                 qser = a.queries + (int64_t)q * n * D;
                 lbtot = lb_m;
                 prefix = T(0);
-                thr = a.abandon ? scale_up<T>(t_thr_raw, a.mg.prune) : INF;
+                thr = a.abandon ? scale_up<T>(t_thr_raw, a.mg) : INF;
                 thr_pend_raw = t_thr_raw;
 #pragma unroll
                 for (int k = 0; k < B; ++k) prev[k] = (k == W) ? T(0) : INF;
@@ -1310,7 +1353,7 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
         if (since >= 8) {
             // the best-so-far read issued 8 rows ago; issue the next one
             since = 0;
-            thr = scale_up<T>(thr_pend_raw, a.mg.prune);
+            thr = scale_up<T>(thr_pend_raw, a.mg);
             if (a.abandon) thr_pend_raw = load_volatile(a.dbest + q);
         }
     };
@@ -1426,6 +1469,7 @@ template <int D, int B, int R, bool CASC, int MINB>
 __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Tiles tl, int64_t n_tiles,
                                                              const uint32_t* __restrict__ cand_of,
                                                              float* __restrict__ res, int* __restrict__ tile_ctr) {
+    n_tiles = tile_count(tl, n_tiles);
     using L = LaneRLayout<D, R>;
     constexpr int W = (B - 1) / 2, DP = L::DP, QGS = L::QGS, EGS = L::EGS, EQ = L::EQ, RD = R * D;
     constexpr int NIT = B + R - 1;              // iterations per step
@@ -1555,7 +1599,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                 crow = a.cands + (int64_t)c_m * n * D;
                 lbtot = lb_m;
                 prefix = 0.f;
-                thr = a.abandon ? scale_up<float>(t_thr_raw, a.mg.prune) : INF;
+                thr = a.abandon ? scale_up<float>(t_thr_raw, a.mg) : INF;
                 thr_pend_raw = t_thr_raw;
 #pragma unroll
                 for (int k = 0; k < B; ++k) ps[k * 32] = (k == W) ? 0.f : INF;
@@ -1690,7 +1734,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                 since += R;
                 if (since >= a.thr_every) {
                     since = 0;
-                    thr = scale_up<float>(thr_pend_raw, a.mg.prune);
+                    thr = scale_up<float>(thr_pend_raw, a.mg);
                     if (a.abandon) thr_pend_raw = load_volatile(a.dbest + cq);
                 }
             }
@@ -1705,7 +1749,6 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     X(6, 13, 4) X(8, 13, 4) X(20, 13, 2) X(5, 103, 4)
 
 static int laner_rows_shape(int n, int d, int B) {  // rows per step for this shape, 0 = not served
-    if (getenv("TCDTW_NO_LANE") || getenv("TCDTW_NO_LANE4")) return 0;
     int rows = 0;
 #define TCDTW_LANER_OK(DD, BB, RR) \
     if (d == DD && B == BB && n % RR == 0) rows = RR;
@@ -1723,7 +1766,6 @@ static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n
                         float* res, int* tctr, cudaStream_t st) {
     constexpr int threads = 64;
     if (laner_rows(a, d, B) == 0) return TCDTW_NOT_SUPPORTED;
-    static const bool no_casc = getenv("TCDTW_NO_CASC") != nullptr;  // A/B switch for benchmarking
     auto go = [&](auto kern, int words_per_warp) -> int {
         const size_t smem = (size_t)(threads / 32) * words_per_warp * sizeof(float);
         int dev = 0, sms = 148, occ = 1;
@@ -1740,7 +1782,7 @@ static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n
         if (grid > need) grid = need;
         cudaMemsetAsync(tctr, 0, sizeof(int), st);
         SArgs<float> a4 = a;
-        if (!getenv("TCDTW_REFILL_MIN")) a4.refill_min = 4;
+        a4.refill_min = 4;  // refill at 2 or 4 free lanes measured equal, 6 and 8 slower (C4)
         kern<<<(int)grid, threads, smem, st>>>(a4, tl, n_tiles, cand_of, res, tctr);
         return launch_status();
     };
@@ -1749,7 +1791,6 @@ static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n
 #define TCDTW_LANER_CASE(DD, BB, RR)                                                          \
     if (d == DD && B == BB && a.n % RR == 0) {                                                \
         const int ww = LaneRLayout<DD, RR>::warp_words(a.n, a.qpad_rows, BB);                 \
-        if (no_casc) return go(dtw_laner_kernel<DD, BB, RR, false, 8>, ww);                   \
         return go(dtw_laner_kernel<DD, BB, RR, true, 8>, ww);                                 \
     }
     TCDTW_LANER_SPECS(TCDTW_LANER_CASE)
@@ -1768,6 +1809,7 @@ template <typename T, int DMAX, bool EXACT>
 __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
                                                        const uint32_t* __restrict__ cand_of, T* __restrict__ res,
                                                        int* __restrict__ tile_ctr) {
+    n_tiles = tile_count(tl, n_tiles);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = a.n, d = a.d, w = a.w, B = 2 * w + 1;
     const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1805,7 +1847,7 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
             const T* crow = a.cands + c * (int64_t)n * d;
             for (int k = lane; k < B; k += 32) prow[k] = (k == w) ? T(0) : INF;
             __syncwarp();
-            T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg.prune) : INF;
+            T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg) : INF;
             T fin = INF;
             bool abandoned = false;
             int stop_row = n - 1;
@@ -1862,7 +1904,7 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
                     stop_row = i0 + first;
                     break;
                 }
-                if (a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg.prune);
+                if (a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg);
             }
             fin = __shfl_sync(0xffffffffu, fin, (n - 1) & 31);
             if (!abandoned && fin > thr) abandoned = true;  // dtw.py:101-102
@@ -1900,33 +1942,54 @@ __host__ inline int wave_row_stride(int es, int d) {
 }
 
 // The same wavefront with the dimension count a compile-time constant and a
-// branch-free step: every lane evaluates its cell (inactive lanes on a
-// clamped query row, the result replaced by +inf), lane 0 takes the row above
-// from the handoff row by a predicated load, and the only synchronisation per
-// step is the shuffle.  The per-step cost drops from ~148 warp instructions
-// (runtime d: address arithmetic, guards, reconvergence) to the DP's own
-// arithmetic plus a few selects (C3: fp64, d = 8).  Row-granular abandoning
-// and the float64 arithmetic order are those of dtw_wave_kernel.
+// branch-free step (C3: d = 8, 2W+1 = 205; the float32 filter's DTW and the
+// float64 EXACT path).  Lane l owns row i0+l of a 32-row chunk and visits its
+// band slot k = tau - 2l at step tau; the cell above arrives from lane l-1 by
+// the one shuffle per step, the diagonal one step later; lane 0 takes the row
+// above from the previous chunk's handoff row.  Per step, per lane:
+//   * the query point at column i0 - l - w + tau comes from the staged query,
+//     padded with +inf rows so that the address only advances by one row per
+//     step (no clamping); lanes outside the band compute on whatever row is
+//     there and their result is replaced by +inf;
+//   * lane 0 reads one handoff slot (the next step's "up" is this step's
+//     "diag"), the handoff row padded with +inf past slot B-1;
+//   * float minima are FMNMX (values are never NaN); float64 minima are
+//     compare-selects (fmin's NaN handling costs four extra instructions).
+// Row-granular abandoning (first row of the chunk whose minimum exceeds the
+// threshold) and the float64 arithmetic order are those of dtw_wave_kernel.
 // QG: the query is read from global memory (L1) instead of being staged --
 // series too long for the staged rows to fit in shared memory.
+template <typename T>
+__device__ __forceinline__ T step_min(T a, T b) {
+    if constexpr (sizeof(T) == 4) return fminf(a, b);
+    else return a < b ? a : b;
+}
+
+constexpr int kWavePad = 32;  // +inf rows before the staged query (lanes trail lane 0 by <= 31 columns)
+__host__ __device__ inline int wave_q_rows(int n, int w) { return n + 2 * w + 2 * kWavePad + 32; }
+__host__ __device__ inline int wave_prow_len(int B) { return B + 66; }  // lane 0 reads slot tau+1 <= B + 63
+
 template <typename T, int D, bool EXACT, bool QG = false>
-__global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
+__global__ void __launch_bounds__(256, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
                                                          const uint32_t* __restrict__ cand_of, T* __restrict__ res,
                                                          int* __restrict__ tile_ctr) {
+    n_tiles = tile_count(tl, n_tiles);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // query rows as whole 16-byte vectors, an odd number of them per row:
     // consecutive lanes read consecutive rows with LDS.128, conflict-free
     // within each quarter warp
     constexpr int SP = WaveRow<T, D>::SP;
     constexpr int VE = WaveRow<T, D>::VE, NV = WaveRow<T, D>::NV;
+    using VT = typename WaveRow<T, D>::VT;
     const int n = a.n, w = a.w, B = 2 * w + 1;
+    const int PR = wave_prow_len(B);
+    const int QR = QG ? 0 : wave_q_rows(n, w);
     const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T* qs = reinterpret_cast<T*>(smem_raw);                          // (n + 2w) * SP
-    T* prow = qs + (QG ? (size_t)0 : (size_t)(n + 2 * w) * SP) + (size_t)wib * (B + 1);  // per warp: B + 1 (last = +inf)
+    T* qs = reinterpret_cast<T*>(smem_raw);                       // QR * SP: row r <-> query column r - w - kWavePad
+    T* prow = qs + (size_t)QR * SP + (size_t)wib * PR;            // per warp handoff row (+inf from slot B on)
     __shared__ int64_t tile_s;
     const T INF = dev_inf<T>();
     const unsigned FULL = 0xffffffffu;
-    const int qmax = n + 2 * w - 1;
     int64_t cached_q = -1;
     while (true) {
         __syncthreads();
@@ -1939,10 +2002,10 @@ __global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
         const int len = tl.len[tile];
         if (!QG && q != cached_q) {
             const T* qsrc = a.queries + q * (int64_t)n * D;
-            for (int e = threadIdx.x; e < (n + 2 * w) * D; e += blockDim.x) {
-                const int r = e / D, p = e - (e / D) * D;
-                const int j = r - w;
-                qs[r * SP + p] = (j >= 0 && j < n) ? qsrc[(int64_t)j * D + p] : INF;
+            for (int e = threadIdx.x; e < QR * SP; e += blockDim.x) {
+                const int r = e / SP, p = e - (e / SP) * SP;
+                const int j = r - w - kWavePad;
+                qs[e] = (p < D && j >= 0 && j < n) ? qsrc[(int64_t)j * D + p] : INF;
             }
             cached_q = q;
             __syncthreads();
@@ -1952,9 +2015,9 @@ __global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
             if (res[ent] < T(0)) continue;  // pruned by the advanced bound (warp-uniform)
             const int64_t c = cand_of[ent];
             const T* crow = a.cands + c * (int64_t)n * D;
-            for (int k = lane; k <= B; k += 32) prow[k] = (k == w) ? T(0) : INF;
+            for (int k = lane; k < PR; k += 32) prow[k] = (k == w) ? T(0) : INF;
             __syncwarp();
-            T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg.prune) : INF;
+            T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg) : INF;
             bool abandoned = false;
             int stop_row = n - 1;
             for (int i0 = 0; i0 < n; i0 += 32) {
@@ -1970,29 +2033,19 @@ __global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
                 const int rows_here = n - i0 < 32 ? n - i0 : 32;
                 const int steps = B + 2 * (rows_here - 1);
                 T mine = INF, got = INF, rmin = INF;
+                T p0 = prow[0];                                          // lane 0: "diag" of step 0
+                const T* qrow = qs + (size_t)(i0 - lane + kWavePad) * SP;  // staged row of step 0
+                T* wrow = prow - 2 * lane;                                // writer: slot tau - 2 lane
                 for (int tau = 0; tau < steps; ++tau) {
-                    const int k = tau - 2 * lane;
-                    const T got_prev = got;
-                    got = __shfl_up_sync(FULL, mine, 1);
-                    const bool act = valid && (unsigned)k < (unsigned)B;
-                    const int kc = k < 0 ? 0 : (k > B - 1 ? B - 1 : k);
-                    T up = got, dg = got_prev;
-                    if (lane == 0) {
-                        up = prow[kc + 1];  // prow[B] = +inf
-                        dg = prow[kc];
-                    }
-                    int qr = i + k;  // padded query row (INF outside [w, w+n))
-                    qr = qr < 0 ? 0 : (qr > qmax ? qmax : qr);
                     T qv[NV * VE];
                     if constexpr (QG) {
-                        const int col = i + k - w;
+                        const int col = i0 - lane - w + tau;
                         const bool in = (unsigned)col < (unsigned)n;
                         const T* src = a.queries + ((int64_t)q * n + (in ? col : 0)) * D;
 #pragma unroll
                         for (int p = 0; p < D; ++p) qv[p] = in ? __ldg(src + p) : INF;
                     } else {
-                        using VT = typename WaveRow<T, D>::VT;
-                        const VT* src = reinterpret_cast<const VT*>(qs + qr * SP);
+                        const VT* src = reinterpret_cast<const VT*>(qrow);
 #pragma unroll
                         for (int v = 0; v < NV; ++v) {
                             const VT x = src[v];
@@ -2006,30 +2059,35 @@ __global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
                                 qv[4 * v + 3] = x.w;
                             }
                         }
+                        qrow += SP;
                     }
-                    const T* qp = qv;
                     T cost;
                     if constexpr (EXACT) {
-                        cost = dist_exact<T, D>(rp, qp, D);
+                        cost = dist_exact<T, D>(rp, qv, D);
                     } else {
-                        T s = T(0);
+                        T sacc = T(0);
 #pragma unroll
                         for (int p = 0; p < D; ++p) {
-                            const T df = rp[p] - qp[p];
-                            s = fma(df, df, s);
+                            const T df = rp[p] - qv[p];
+                            sacc = fma(df, df, sacc);
                         }
-                        cost = fast_sqrt(s);
+                        cost = fast_sqrt(sacc);
                     }
-                    // compare-select minima: the operands are never NaN
-                    // (fmin's NaN handling costs four extra instructions per
-                    // double minimum); equal operands are equal values
-                    const T m1 = dg < up ? dg : up;
-                    const T best = mine < m1 ? mine : m1;
+                    const T got_prev = got;
+                    got = __shfl_up_sync(FULL, mine, 1);
+                    T up = got, dg = got_prev;
+                    if (lane == 0) {
+                        up = prow[tau + 1];  // +inf past the band
+                        dg = p0;
+                        p0 = up;
+                    }
+                    const bool act = valid && (unsigned)(tau - 2 * lane) < (unsigned)B;
+                    const T best = step_min(step_min(dg, up), mine);
                     T v = EXACT ? add_rn(cost, best) : cost + best;
                     v = act ? v : INF;
-                    rmin = v < rmin ? v : rmin;
+                    rmin = step_min(rmin, v);
                     mine = v;
-                    if (act && writer) prow[k] = v;
+                    if (act && writer) wrow[tau] = v;
                 }
                 __syncwarp();  // the handoff row is complete for the next chunk
                 const unsigned bad = __ballot_sync(FULL, valid && rmin > thr);
@@ -2038,7 +2096,7 @@ __global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
                     stop_row = i0 + __ffs(bad) - 1;
                     break;
                 }
-                if (a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg.prune);
+                if (a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg);
             }
             const T fin = abandoned ? INF : prow[w];  // row n-1, column n-1
             if (!abandoned && fin > thr) abandoned = true;  // dtw.py:101-102
@@ -2062,151 +2120,6 @@ __global__ void __launch_bounds__(384, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
 // dimension counts with a compile-time wavefront kernel
 #define TCDTW_WAVE_DIMS(X) X(3) X(4) X(5) X(6) X(8)
 
-// ------------------- DTW, warp per pair, continuous row pipeline (W >= 32)
-// Lane l owns rows l, l+32, l+64, ...; row r = l + 32m sweeps its 2W+1 band
-// columns in consecutive steps starting at S(r) = m(2W+1) + 2l, so lanes stay
-// busy back to back (no drain between 32-row chunks when 2W+1 >= 64).  The
-// cell above comes from lane l-1 one step earlier (one shuffle), the diagonal
-// from two steps earlier; lane 0 reads row r-1 (lane 31's previous row) from
-// a per-warp handoff row in shared memory.  Query rows are staged once per
-// block tile with an odd word stride (conflict-free column reads).  Rows
-// finish strictly in order, one per step at most, so the first row whose
-// minimum exceeds the threshold is found exactly (row-granular abandoning).
-template <typename T>
-__host__ __device__ inline int pipe_stride(int d) {  // odd number of 4-byte words per query row
-    if (sizeof(T) == 4) return (d % 2 == 1) ? d : d + 1;
-    return (d % 2 == 1) ? d : d + 1;  // doubles: odd count of 8-byte words
-}
-
-template <typename T, int DMAX, bool EXACT>
-__global__ void __launch_bounds__(256) dtw_pipe_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
-                                                       const uint32_t* __restrict__ cand_of, T* __restrict__ res,
-                                                       int* __restrict__ tile_ctr) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int n = a.n, d = a.d, w = a.w, B = 2 * w + 1;
-    const int SP = pipe_stride<T>(d);
-    const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T* qs = reinterpret_cast<T*>(smem_raw);                  // n * SP
-    T* hb = qs + (size_t)n * SP + (size_t)wib * (n + 1);     // per warp: row r-1 for lane 0 (index j+1)
-    __shared__ int64_t tile_s;
-    const T INF = dev_inf<T>();
-    const unsigned FULL = 0xffffffffu;
-    const int src = (lane + 31) & 31;
-    int64_t cached_q = -1;
-    while (true) {
-        __syncthreads();
-        if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1);
-        __syncthreads();
-        const int64_t tile = tile_s;
-        if (tile >= n_tiles) break;
-        const int64_t q = tl.q[tile];
-        const int64_t e0 = tl.begin[tile];
-        const int len = tl.len[tile];
-        if (q != cached_q) {
-            const T* qsrc = a.queries + q * (int64_t)n * d;
-            for (int e = threadIdx.x; e < n * d; e += blockDim.x) {
-                const int r = e / d, p = e - (e / d) * d;
-                qs[r * SP + p] = qsrc[e];
-            }
-            cached_q = q;
-            __syncthreads();
-        }
-        for (int slot = wib; slot < len; slot += warps) {
-            const int64_t ent = e0 + slot;
-            if (res[ent] < T(0)) continue;  // pruned by the advanced bound (warp-uniform)
-            const int64_t c = cand_of[ent];
-            const T* crow = a.cands + c * (int64_t)n * d;
-            T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg.prune) : INF;
-            int r = lane;                 // this lane's current row
-            int k = -2 * lane;            // slot within the row (negative: not started)
-            T rp[DMAX], rnext[DMAX];
-            load_point<T, DMAX>(rp, crow + (int64_t)(r < n ? r : 0) * d, d);
-            load_point<T, DMAX>(rnext, crow + (int64_t)(r + 32 < n ? r + 32 : 0) * d, d);
-            T mine = INF, got = INF, rmin = INF, fin = INF;
-            bool abandoned = false;
-            int stop_row = n - 1;
-            const int last_step = ((n - 1) / 32) * B + 2 * ((n - 1) & 31) + B;  // step after row n-1 ends
-            for (int tau = 0; tau < last_step; ++tau) {
-                const T got_prev = got;
-                got = __shfl_sync(FULL, mine, src);
-                const bool act = r < n && k >= 0;
-                T v = INF;
-                if (act) {
-                    const int j = r - w + k;
-                    T up, dg;
-                    if (lane == 0) {
-                        up = (r > 0 && k < B - 1 && j >= 0 && j < n) ? hb[j + 1] : INF;
-                        dg = (r > 0 && j >= 1 && j <= n) ? hb[j] : INF;
-                    } else {
-                        up = (k < B - 1) ? got : INF;
-                        dg = got_prev;
-                    }
-                    T best = tmin(tmin(up, dg), (k > 0) ? mine : INF);
-                    if (r == 0 && j == 0) best = T(0);
-                    T cost = INF;
-                    if (j >= 0 && j < n) {
-                        const T* qp = qs + j * SP;
-                        if constexpr (EXACT) {
-                            cost = dist_exact<T, DMAX>(rp, qp, d);
-                        } else {
-                            T s2 = T(0);
-#pragma unroll
-                            for (int p = 0; p < DMAX; ++p)
-                                if (p < d) {
-                                    const T df = rp[p] - qp[p];
-                                    s2 = fma(df, df, s2);
-                                }
-                            cost = fast_sqrt(s2);
-                        }
-                    }
-                    v = EXACT ? add_rn(cost, best) : cost + best;
-                    rmin = tmin(rmin, v);
-                    if (r == n - 1 && k == w) fin = v;
-                }
-                __syncwarp();
-                if (act && lane == 31 && r - w + k >= 0 && r - w + k < n) hb[r - w + k + 1] = v;  // to lane 0's next row
-                __syncwarp();
-                mine = v;
-                // row end: abandon test (rows end in order, at most one per step)
-                const bool row_end = act && k == B - 1;
-                const bool bad = row_end && rmin > thr;
-                const unsigned badm = __ballot_sync(FULL, bad);
-                if (badm) {
-                    abandoned = true;
-                    stop_row = __shfl_sync(FULL, r, __ffs(badm) - 1);
-                    break;
-                }
-                if (act) ++k;
-                else if (k < 0) ++k;
-                if (k == B) {  // next row of this lane
-                    k = 0;
-                    r += 32;
-                    rmin = INF;  // (mine keeps the last cell: lane l+1 still needs it next step)
-#pragma unroll
-                    for (int p = 0; p < DMAX; ++p) rp[p] = rnext[p];
-                    if (r + 32 < n) load_point<T, DMAX>(rnext, crow + (int64_t)(r + 32) * d, d);
-                }
-                if ((tau & 63) == 63 && a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg.prune);
-            }
-            fin = __shfl_sync(FULL, fin, (n - 1) & 31);
-            if (!abandoned && fin > thr) abandoned = true;  // dtw.py:101-102
-            if (lane == 0) {
-                res[ent] = abandoned ? INF : fin;
-                if (!abandoned) {
-                    atomic_min_nonneg<T>(a.dbest + q, fin);
-                    note_done(a, q, ent);
-                }
-                int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
-                atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_DTW_COMPUTED), 1ull);
-                if (abandoned) atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_ABANDON_COUNT), 1ull);
-                atomicAdd(reinterpret_cast<unsigned long long*>(ctr + TCDTW_C_DTW_CELLS),
-                          (unsigned long long)cells_upto(stop_row, n, w));
-            }
-            __syncwarp();
-        }
-    }
-}
-
 // ------------------------------------------------- advanced bounds (step 2)
 // One lane per survivor, the tile's query shared by the warp; evaluated only
 // in the trigger band LB_MV > e * d_best (search.py:147).  A survivor whose
@@ -2220,6 +2133,7 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
                                                        const uint32_t* __restrict__ cand_of, T* __restrict__ res,
                                                        T* __restrict__ ti_scratch, int* __restrict__ tile_ctr,
                                                        bool ring_smem) {
+    n_tiles = tile_count(tl, n_tiles);
     extern __shared__ __align__(16) unsigned char adv_smem[];
     const int n = a.n, d = a.d, w = a.w, B = 2 * w + 1;
     const int lane = threadIdx.x & 31;
@@ -2235,7 +2149,7 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
         const bool has = lane < tl.len[tile];
         const int64_t c = has ? (int64_t)cand_of[ent] : 0;
         const T db = load_volatile(a.dbest + q);
-        const T thr = scale_up<T>(db, a.mg.prune);
+        const T thr = scale_up<T>(db, a.mg);
         const T lb1 = has ? a.lb[q * a.N + c] : T(0);
         // trigger band: b1 > e * d_best (search.py:147); EXACT uses the
         // reference's float64 product
@@ -2407,6 +2321,7 @@ template <typename T, int D, bool VEC>
 __global__ void __launch_bounds__(256) advanced_pc_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
                                                           const uint32_t* __restrict__ cand_of, T* __restrict__ res,
                                                           int* __restrict__ tile_ctr) {
+    n_tiles = tile_count(tl, n_tiles);
     using T2 = typename Vec8<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = a.n, G = a.G, K = a.K, gw = a.gw;
@@ -2433,7 +2348,7 @@ __global__ void __launch_bounds__(256) advanced_pc_kernel(SArgs<T> a, Tiles tl, 
         }
         const int64_t c = has ? (int64_t)cand_of[ent] : 0;
         const T db = load_volatile(a.dbest + q);
-        const T thr = scale_up<T>(db, a.mg.prune);
+        const T thr = scale_up<T>(db, a.mg);
         const T lb1 = has ? a.lb[q * a.N + c] : T(0);
         const bool go = has && !(res[ent] < T(0)) && (lb1 > a.trigger * db);  // trigger band, search.py:147
         const T* crow = a.cands + c * (int64_t)n * D;
@@ -2524,6 +2439,7 @@ static int launch_advanced_pc(const SArgs<T>& a, int d, Tiles tl, int64_t n_tile
 template <typename T>
 __global__ void fin_min_kernel(Tiles tl, int64_t n_tiles, const T* __restrict__ res, T* __restrict__ minv,
                                const unsigned long long* __restrict__ done_cnt, int64_t done_cap) {
+    n_tiles = tile_count(tl, n_tiles);
     if (done_cnt && (int64_t)*done_cnt <= done_cap) return;  // the completed list covers it
     for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
          tile += (int64_t)gridDim.x * (blockDim.x >> 5)) {
@@ -2608,10 +2524,11 @@ __device__ __forceinline__ void rescore_entry(const SArgs<T>& a, int64_t q, int6
     } else {
         T bound = minv[q];
         if (dbest_in) bound = tmin(bound, dbest_in[q]);
-        const T thr = __fmul_ru(bound, a.mg.fin);
+        const T thr = fin_up(bound, a.mg);
         if (!(r <= thr)) return;
-        const double d64 = dtw_exact_thread<DMAX, T>(a.queries + q * (int64_t)a.n * a.d,
-                                                    a.cands + (int64_t)c * a.n * a.d, a.n, a.d, a.w, my_scratch);
+        const int64_t qo = q * (int64_t)a.n * a.d, co = (int64_t)c * a.n * a.d;
+        const double d64 = a.xq ? dtw_exact_thread<DMAX, double>(a.xq + qo, a.xc + co, a.n, a.d, a.w, my_scratch)
+                                : dtw_exact_thread<DMAX, T>(a.queries + qo, a.cands + co, a.n, a.d, a.w, my_scratch);
         const unsigned long long bits = (unsigned long long)__double_as_longlong(d64);
         if (pass == 0) {
             atomicMin(min64 + q, bits);
@@ -2628,6 +2545,7 @@ __global__ void fin_rescore_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles, const 
                                    int pass, unsigned long long* __restrict__ min64,
                                    unsigned long long* __restrict__ best_idx, double* __restrict__ scratch,
                                    const unsigned long long* __restrict__ done_cnt, int64_t done_cap) {
+    n_tiles = tile_count(tl, n_tiles);
     if (done_cnt && (int64_t)*done_cnt <= done_cap) return;  // the completed list covers it
     const int lane = threadIdx.x & 31;
     const int64_t gthread = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -2697,7 +2615,7 @@ __device__ __forceinline__ void collect_entry(const SArgs<T>& a, int64_t q, T r,
     } else {
         T bound = minv[q];
         if (dbest_in) bound = tmin(bound, dbest_in[q]);
-        take = r <= __fmul_ru(bound, a.mg.fin);
+        take = r <= fin_up(bound, a.mg);
     }
     if (!take) return;
     const unsigned long long k = atomicAdd(f.cnt, 1ull);
@@ -2736,73 +2654,119 @@ __global__ void fin_collect_kernel(SArgs<T> a, Tiles stl, int64_t n_seed_tiles, 
 
 // EXACT float64 DTW of one (query, candidate) pair by one warp: lane = row of
 // a 32-row chunk, anti-diagonal skew of 2 per lane, one shuffle per step, the
-// chunk's last row handed over through shared memory (prow, 2W+1 doubles).
-// Same per-cell arithmetic as dtw_banded (numpy order, no contraction).
-template <typename TIn, int DMAX>
-__device__ double dtw_warp_exact(const TIn* __restrict__ rows_s, const TIn* __restrict__ cols_s, int n, int d,
-                                 int w, double* prow) {
+// chunk's last row handed over through shared memory (prow, 2W+2 doubles, the
+// last one +inf).  Same per-cell arithmetic as dtw_banded (numpy order, no
+// contraction).  Branch-free steps with the NEXT step's cell cost computed
+// ahead, so the correctly rounded square root (the long pole) overlaps the
+// min/add recurrence instead of sitting on it; lanes outside the band work
+// on clamped indices and their result is replaced by +inf.
+template <typename TIn, typename TCol, int DMAX, bool VEC = false>
+__device__ double dtw_warp_exact(const TIn* __restrict__ rows_s, const TCol* __restrict__ cols_s, int col_stride,
+                                 int n, int d, int w, double* prow) {
     const int lane = threadIdx.x & 31;
     const int B = 2 * w + 1;
     const double INF = dev_inf<double>();
-    for (int k = lane; k < B; k += 32) prow[k] = (k == w) ? 0.0 : INF;
+    const unsigned FULL = 0xffffffffu;
+    for (int k = lane; k <= B; k += 32) prow[k] = (k == w) ? 0.0 : INF;
     __syncwarp();
-    double fin = INF;
     for (int i0 = 0; i0 < n; i0 += 32) {
         const int i = i0 + lane;
         const bool valid = i < n;
+        const bool writer = valid && (lane == 31 || i == n - 1);
         double rp[DMAX];
+        {
+            const TIn* src = rows_s + (int64_t)(valid ? i : n - 1) * d;
 #pragma unroll
-        for (int p = 0; p < DMAX; ++p) rp[p] = (valid && p < d) ? (double)rows_s[(int64_t)i * d + p] : 0.0;
+            for (int p = 0; p < DMAX; ++p) rp[p] = p < d ? (double)src[p] : 0.0;
+        }
+        // cost of this lane's cell at step tau: slot k = tau - 2 lane
+        auto cost_at = [&](int tau) -> double {
+            const int k = tau - 2 * lane;
+            const int j = i - w + k;
+            const bool in = valid && (unsigned)k < (unsigned)B && (unsigned)j < (unsigned)n;
+            const TCol* col = cols_s + (int64_t)(in ? j : 0) * col_stride;
+            double cv[DMAX];
+            if constexpr (VEC && sizeof(TCol) == 8) {  // staged rows: 16-byte aligned, odd 16-byte stride
+#pragma unroll
+                for (int p = 0; p + 1 < DMAX; p += 2) {
+                    if (p + 1 < d) {
+                        const double2 v2 = *reinterpret_cast<const double2*>(col + p);
+                        cv[p] = v2.x;
+                        cv[p + 1] = v2.y;
+                    } else if (p < d) {
+                        cv[p] = (double)col[p];
+                    }
+                }
+                if (DMAX % 2 == 1 && DMAX - 1 < d) cv[DMAX - 1] = (double)col[DMAX - 1];
+            } else {
+#pragma unroll
+                for (int p = 0; p < DMAX; ++p)
+                    if (p < d) cv[p] = (double)col[p];
+            }
+            double sq[DMAX];
+#pragma unroll
+            for (int p = 0; p < DMAX; ++p) {
+                if (p < d) {
+                    const double df = __dsub_rn(rp[p], cv[p]);
+                    sq[p] = __dmul_rn(df, df);
+                } else {
+                    sq[p] = 0.0;
+                }
+            }
+            const double c = __dsqrt_rn(np_sum<double, DMAX>(sq, d));
+            return in ? c : INF;
+        };
+        const int rows_here = n - i0 < 32 ? n - i0 : 32;
+        const int steps = B + 2 * (rows_here - 1);
         double mine = INF, got = INF;
-        const int steps = B + 62;
+        double cost = cost_at(0);
         for (int tau = 0; tau < steps; ++tau) {
+            const double cost_next = cost_at(tau + 1);  // independent of the recurrence below
             const int k = tau - 2 * lane;
             const double got_prev = got;
-            got = __shfl_up_sync(0xffffffffu, mine, 1);
-            const bool act = valid && k >= 0 && k < B;
-            double v = INF;
-            if (act) {
-                double up, dg;
-                if (lane == 0) {
-                    up = (k + 1 < B) ? prow[k + 1] : INF;
-                    dg = prow[k];
-                } else {
-                    up = got;
-                    dg = got_prev;
-                }
-                const int j = i - w + k;
-                double cost = INF;
-                if (j >= 0 && j < n) {
-                    double sq[DMAX];
-#pragma unroll
-                    for (int p = 0; p < DMAX; ++p) {
-                        if (p < d) {
-                            const double df = __dsub_rn(rp[p], (double)cols_s[(int64_t)j * d + p]);
-                            sq[p] = __dmul_rn(df, df);
-                        } else {
-                            sq[p] = 0.0;
-                        }
-                    }
-                    cost = __dsqrt_rn(np_sum<double, DMAX>(sq, d));
-                }
-                const double best = fmin(fmin(up, dg), mine);
-                v = __dadd_rn(cost, best);
-                if (i == n - 1 && k == w) fin = v;
+            got = __shfl_up_sync(FULL, mine, 1);
+            const bool act = valid && (unsigned)k < (unsigned)B;
+            const int kc = k < 0 ? 0 : (k > B - 1 ? B - 1 : k);
+            double up = got, dg = got_prev;
+            if (lane == 0) {
+                up = prow[kc + 1];  // prow[B] = +inf
+                dg = prow[kc];
             }
+            // compare-select minima: never NaN, equal operands are equal values
+            const double m1 = dg < up ? dg : up;
+            const double best = mine < m1 ? mine : m1;
+            double v = __dadd_rn(cost, best);
+            v = act ? v : INF;
             mine = v;
-            __syncwarp();
-            if (act && lane == 31) prow[k] = v;
-            __syncwarp();
+            if (act && writer) prow[k] = v;
+            cost = cost_next;
         }
+        __syncwarp();  // the handoff row is complete for the next chunk
     }
-    return __shfl_sync(0xffffffffu, fin, (n - 1) & 31);
+    const double fin = prow[w];  // row n-1, column n-1
+    __syncwarp();
+    return fin;
 }
 
-template <typename T, int DMAX>
+// Doubles per staged query point: pairs of doubles (16 bytes), an odd number
+// of them, so lanes reading consecutive points with 16-byte loads do not
+// conflict.
+__host__ __device__ inline int rescore_col_stride(int d) {
+    const int units = (d + 1) / 2;
+    return 2 * (units % 2 == 1 ? units : units + 1);
+}
+
+// One warp per finalist.  STAGE: the finalist's query (the DP's columns,
+// read at every step) is first copied into the warp's shared memory as
+// float64 with rescore_col_stride; else it is read from global memory.
+template <typename T, int DMAX, bool STAGE>
 __global__ void fin_rescore_warp_kernel(SArgs<T> a, Finalists f, unsigned long long* __restrict__ min64) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* prow = reinterpret_cast<double*>(smem_raw) + (size_t)wib * (2 * a.w + 1);
+    const int cs = rescore_col_stride(a.d);
+    const size_t per_warp = (STAGE ? (size_t)a.n * cs : 0) + (size_t)(2 * a.w + 2);
+    double* qs = reinterpret_cast<double*>(smem_raw) + (size_t)wib * per_warp;
+    double* prow = qs + (STAGE ? (size_t)a.n * cs : 0);
     const int64_t cnt = min((int64_t)*f.cnt, f.cap);
     for (int64_t k = blockIdx.x * (int64_t)warps + wib; k < cnt; k += (int64_t)gridDim.x * warps) {
         const unsigned long long x = f.item[k];
@@ -2811,9 +2775,22 @@ __global__ void fin_rescore_warp_kernel(SArgs<T> a, Finalists f, unsigned long l
         if constexpr (sizeof(T) == 8) {
             d64 = f.d64[k];  // EXACT: the stored value is the reference's
         } else {
-            // DTW is symmetric (test_dtw.py:196-207): rows = candidate
-            d64 = dtw_warp_exact<T, DMAX>(a.cands + c * (int64_t)a.n * a.d, a.queries + q * (int64_t)a.n * a.d,
-                                          a.n, a.d, a.w, prow);
+            // DTW is symmetric (test_dtw.py:196-207): rows = candidate.  With
+            // the float32 filter on float64 data, the float64 originals.
+            const int64_t qo = q * (int64_t)a.n * a.d, co = c * (int64_t)a.n * a.d;
+            if constexpr (STAGE) {
+                __syncwarp();
+                for (int e = lane; e < a.n * a.d; e += 32) {
+                    const int r = e / a.d, p = e - r * a.d;
+                    qs[r * cs + p] = a.xq ? a.xq[qo + e] : (double)a.queries[qo + e];
+                }
+                __syncwarp();
+                d64 = a.xq ? dtw_warp_exact<double, double, DMAX, true>(a.xc + co, qs, cs, a.n, a.d, a.w, prow)
+                           : dtw_warp_exact<T, double, DMAX, true>(a.cands + co, qs, cs, a.n, a.d, a.w, prow);
+            } else {
+                d64 = a.xq ? dtw_warp_exact<double, double, DMAX>(a.xc + co, a.xq + qo, a.d, a.n, a.d, a.w, prow)
+                           : dtw_warp_exact<T, T, DMAX>(a.cands + co, a.queries + qo, a.d, a.n, a.d, a.w, prow);
+            }
         }
         if (lane == 0) {
             f.d64[k] = d64;
@@ -2885,12 +2862,51 @@ __global__ void alu_probe_kernel(int iters, T* sink) {
     if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == T(-1)) sink[0] = a0;
 }
 
+// ------------------------------------------- float32 filter on float64 data
+// Rounded float32 copy of (points, d) float64 values and the largest squared
+// point norm (nonnegative doubles order like their bit patterns).
+static __global__ void round_points_kernel(const double* __restrict__ in, int64_t points, int d, float* __restrict__ out,
+                                    unsigned long long* __restrict__ max_sq_bits) {
+    double mx = 0.0;
+    for (int64_t pt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pt < points;
+         pt += (int64_t)gridDim.x * blockDim.x) {
+        const double* x = in + pt * d;
+        float* y = out + pt * d;
+        double s = 0.0;
+        for (int k = 0; k < d; ++k) {
+            const double v = x[k];
+            y[k] = __double2float_rn(v);
+            s = fma(v, v, s);
+        }
+        mx = fmax(mx, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(max_sq_bits, (unsigned long long)__double_as_longlong(mx));
+}
+
+// Additive slack of the float32 decisions.  Rounding a point x to float32
+// moves it by at most 2^-24 |x|, so one cell cost moves by at most
+// 2^-24 (|q| + |c|) and any warping path (<= 2n-1 cells), hence DTW and
+// every bound, by A = (2n-1) 2^-24 (max|q| + max|c|).  A prune / abandon
+// decision compares a bound of one candidate with the DTW of another, and a
+// finalist is kept against the best: both need 2A, kept with 25% to spare.
+static __global__ void f32_slack_kernel(const unsigned long long* __restrict__ max_sq_bits, int n, float* __restrict__ add) {
+    const double qn = sqrt(__longlong_as_double((long long)max_sq_bits[0]));
+    const double cn = sqrt(__longlong_as_double((long long)max_sq_bits[1]));
+    const double A = (2.0 * n - 1.0) * 5.9604644775390625e-08 * (qn + cn) * (1.0 + 1e-6) + 1e-30;
+    add[0] = __double2float_ru(2.5 * A);
+    add[1] = __double2float_ru(2.5 * A);
+}
+
 // =================================================================== plan
 struct Plan {
     int64_t Q, N;
     int n, d, w, B, G, K, S, n_chunks;
     size_t es;  // element size
     bool has_lb, exact, rev;
+    bool f32f;  // TCDTW_FLAG_F32_FILTER: float64 inputs, float32 filter
+    size_t o_q32, o_c32, o_slack;
     int64_t max_tiles;
     // byte offsets
     size_t o_qT, o_ub, o_done, o_fin;
@@ -2930,11 +2946,14 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     p.B = 2 * p.w + 1;
     p.G = (p.n - 1) / dsc->group_width + 1;
     p.K = dsc->max_boxes;
-    p.exact = dsc->dtype == TCDTW_F64;
+    p.f32f = (dsc->flags & TCDTW_FLAG_F32_FILTER) != 0;
+    if (p.f32f && dsc->dtype != TCDTW_F64) return TCDTW_INVALID_INPUT;
+    p.exact = dsc->dtype == TCDTW_F64 && !p.f32f;
     p.es = p.exact ? 8 : 4;
     p.has_lb = dsc->method != TCDTW_METHOD_NONE;
     p.rev = p.has_lb && (dsc->flags & TCDTW_FLAG_REVERSE_LB) != 0;
     if (p.rev && (!dsc->cand_upper || !dsc->cand_lower)) return TCDTW_INVALID_INPUT;
+    if (p.rev && p.f32f) return TCDTW_NOT_SUPPORTED;
     p.S = p.has_lb ? (dsc->seeds > 0 ? dsc->seeds : 8) : 0;
     if (p.S > kSeedMax) return TCDTW_INVALID_INPUT;
     if (p.S > p.N) p.S = (int)p.N;
@@ -2999,7 +3018,7 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
         const int64_t rem = N % ((int64_t)p.ub_ct * p.ub_stride);
         p.ub_sampled = full + (rem < p.ub_ct ? rem : p.ub_ct);
     }
-    if (const char* cap = getenv("TCDTW_DONE_CAP")) p.done_cap = atoll(cap);  // tests: force the overflow path
+    if (dsc->done_cap > 0) p.done_cap = dsc->done_cap;  // tests force the overflow path with 1
     p.o_done = take((size_t)p.done_cap * 8 + 64);
     p.fin_cap = p.done_cap + Q * kSeedMax;
     p.o_fin = take((size_t)p.fin_cap * 16 + 64);
@@ -3014,6 +3033,9 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     const bool ti = dsc->method == TCDTW_METHOD_LB_TI ||
                     (dsc->method == TCDTW_METHOD_TC_DTW && dsc->advanced == TCDTW_METHOD_LB_TI);
     p.o_tisc = take(ti ? (size_t)p.adv_warps * 32 * 3 * p.B * es : 0);
+    p.o_q32 = take(p.f32f ? series_q : 0);
+    p.o_c32 = take(p.f32f ? (size_t)N * p.n * p.d * 4 : 0);
+    p.o_slack = take(p.f32f ? 32 : 0);
     p.qpad_rows = p.n + 2 * p.w + 8;
     p.o_qpad = take(p.exact ? 0 : (size_t)Q * p.qpad_rows * ((p.d + 1) / 2) * 8);
     p.total = o;
@@ -3059,10 +3081,9 @@ static int sm_count() {
         if (_s != TCDTW_OK) return _s; \
     } while (0)
 
-// TCDTW_DEBUG=1: synchronise and report after every pipeline stage.
-static void dbg_stage(cudaStream_t st, const char* what) {
-    static const bool on = getenv("TCDTW_DEBUG") != nullptr;
-    if (!on) return;
+// TCDTW_FLAG_DEBUG_SYNC: synchronise and report after every pipeline stage.
+static void dbg_stage(const tcdtw_search_desc* dsc, cudaStream_t st, const char* what) {
+    if (!(dsc->flags & TCDTW_FLAG_DEBUG_SYNC)) return;
     cudaError_t e = cudaStreamSynchronize(st);
     fprintf(stderr, "[tcdtw] %-24s %s\n", what, cudaGetErrorString(e));
     fflush(stderr);
@@ -3115,13 +3136,21 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
     }
     a.abandon = dsc->method != TCDTW_METHOD_NONE;
     a.refill_min = 8;
-    a.thr_every = getenv("TCDTW_THR_EVERY") ? atoi(getenv("TCDTW_THR_EVERY")) : 8;
-    if (const char* rm = getenv("TCDTW_REFILL_MIN")) a.refill_min = atoi(rm);
+    a.thr_every = 8;  // re-reading the live d_best every 4 / 8 / 16 rows measured equal (C4)
     a.done_list = nullptr;  // set for the survivors pass only
     a.done_cnt = nullptr;
     a.done_cap = 0;
     a.qpad = p.exact ? nullptr : at<float2>(ws, p.o_qpad);
     a.qpad_rows = p.qpad_rows;
+    a.mg.add = nullptr;
+    a.xq = a.xc = nullptr;
+    if (p.f32f) {  // queries / cands are the float32 copies in the workspace
+        a.queries = at<T>(ws, p.o_q32);
+        a.cands = at<T>(ws, p.o_c32);
+        a.xq = (const double*)queries;
+        a.xc = (const double*)cands;
+        a.mg.add = at<float>(ws, p.o_slack);
+    }
     return a;
 }
 
@@ -3134,16 +3163,15 @@ static int launch_wave_d(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_t
     cudaMemsetAsync(tctr, 0, sizeof(int), st);
     // the query rows are shared by the block's warps; block size 256 (or
     // TCDTW_WAVE_THREADS=384: registers are capped for two such blocks)
-    const size_t q_bytes = (size_t)(p.n + 2 * p.w) * wave_row_stride((int)sizeof(T), p.d) * sizeof(T);
+    const size_t q_bytes = (size_t)wave_q_rows(p.n, p.w) * wave_row_stride((int)sizeof(T), p.d) * sizeof(T);
+    const size_t prow_bytes = (size_t)wave_prow_len(p.B) * sizeof(T);
     auto run_d = [&](auto kern) -> int {
         int best_t = 0, best_w = 0;
         size_t best_s = 0;
         // 384-thread blocks keep 24 warps resident but split each 32-pair
-        // tile unevenly (C3: 2717 vs 3131 q/s at 256): 256 unless overridden
-        static const int force_t = getenv("TCDTW_WAVE_THREADS") ? atoi(getenv("TCDTW_WAVE_THREADS")) : 256;
-        for (int t = 256; t <= 384; t += 128) {
-            if (force_t && t != force_t) continue;
-            const size_t sm = q_bytes + (size_t)(t / 32) * (p.B + 1) * sizeof(T);
+        // tile unevenly (C3: 2717 vs 3131 q/s at 256): 256
+        for (int t = 256; t <= 256; t += 128) {
+            const size_t sm = q_bytes + (size_t)(t / 32) * prow_bytes;
             if (sm > 227 * 1024) continue;
             if (sm > 48 * 1024 &&
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
@@ -3163,12 +3191,12 @@ static int launch_wave_d(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_t
         return launch_status();
     };
     // staged query rows too large for shared memory: read them through L1
-    const bool qg = q_bytes + (size_t)8 * (p.B + 1) * sizeof(T) > 227 * 1024;
+    const bool qg = q_bytes + (size_t)8 * prow_bytes > 227 * 1024;
 #define TCDTW_WAVE_CASE(DD)                                                                           \
     if (p.d == DD && DD <= DMAX) {                                                                    \
         if (qg) {                                                                                     \
             auto kq = dtw_wave_d_kernel<T, (DD <= DMAX ? DD : 1), EXACT, true>;                       \
-            const size_t sm = (size_t)8 * (p.B + 1) * sizeof(T);                                      \
+            const size_t sm = (size_t)8 * prow_bytes;                                                 \
             if (sm > 48 * 1024 &&                                                                     \
                 cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) \
                 return TCDTW_NOT_SUPPORTED;                                                           \
@@ -3191,28 +3219,24 @@ static int launch_wave_d(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_t
 // per-pair latency of the lane kernels (one lane walks all n rows) dominates,
 // so the warp-per-pair wavefront (about n + 2W dependent steps) runs instead.
 static inline bool few_pairs(int64_t pairs_upper) {
-    static const bool off = getenv("TCDTW_NO_SMALL_WAVE") != nullptr;  // A/B switch
-    return !off && pairs_upper <= (int64_t)sm_count() * 8;
+    return pairs_upper <= (int64_t)sm_count() * 8;
 }
 
 // DTW launcher over a tile list: thread-per-pair if the band fits the
 // register buckets, else the wavefront kernel.
 template <typename T, int DMAX, bool EXACT>
 static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tiles, const uint32_t* cand_of, T* res,
-                      int* tctr, cudaStream_t st) {
+                      int* tctr, cudaStream_t st, bool few) {
     if (n_tiles <= 0) return TCDTW_OK;
-    if (few_pairs(n_tiles * (int64_t)kTile) && !getenv("TCDTW_WAVE_GENERIC")) {
+    if (few) {
         const int s = launch_wave_d<T, DMAX, EXACT>(a, p, tl, n_tiles, cand_of, res, tctr, st);
         if (s != TCDTW_NOT_SUPPORTED) return s;
     }
-    const bool no_lane = getenv("TCDTW_NO_LANE") != nullptr;  // A/B switch for benchmarking
     if constexpr (!EXACT) {
-        if (!no_lane && getenv("TCDTW_NO_LANE4") == nullptr) {
-            const int s = launch_laner(a, p.d, p.B, tl, n_tiles, cand_of, res, tctr, st);
-            if (s != TCDTW_NOT_SUPPORTED) return s;
-        }
+        const int s = launch_laner(a, p.d, p.B, tl, n_tiles, cand_of, res, tctr, st);
+        if (s != TCDTW_NOT_SUPPORTED) return s;
     }
-    if (!no_lane) {
+    {
         const int s = launch_lane<T>(a, p.d, p.B, tl, n_tiles, cand_of, res, tctr, st);
         if (s != TCDTW_NOT_SUPPORTED) return s;
     }
@@ -3240,24 +3264,7 @@ static int launch_dtw(const SArgs<T>& a, const Plan& p, Tiles tl, int64_t n_tile
         if (p.B <= 32) return run(dtw_tpp_kernel<T, DMAX, 32, EXACT>);
         return run(dtw_tpp_kernel<T, DMAX, 64, EXACT>);
     }
-    // continuous row pipeline: correct (tests/test_gpu_parity.py::test_long_band_shapes)
-    // but measured slower than the chunked wavefront on C1b/C3; opt-in
-    const bool use_pipe = getenv("TCDTW_PIPE") != nullptr;
-    if (p.w >= 32 && use_pipe) {
-        const size_t smem = ((size_t)p.n * pipe_stride<T>(p.d) + (size_t)8 * (p.n + 1)) * sizeof(T);
-        auto kern = dtw_pipe_kernel<T, DMAX, EXACT>;
-        if (smem > 48 * 1024 &&
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return TCDTW_NOT_SUPPORTED;
-        int occ = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
-        if (occ < 1) return TCDTW_NOT_SUPPORTED;
-        int64_t grid = (int64_t)occ * sms;
-        if (grid > n_tiles) grid = n_tiles;
-        kern<<<(int)grid, 256, smem, st>>>(a, tl, n_tiles, cand_of, res, tctr);
-        return launch_status();
-    }
-    if (!getenv("TCDTW_WAVE_GENERIC")) {  // A/B switch
+    {
         const int s = launch_wave_d<T, DMAX, EXACT>(a, p, tl, n_tiles, cand_of, res, tctr, st);
         if (s != TCDTW_NOT_SUPPORTED) return s;
     }
@@ -3285,6 +3292,25 @@ struct SearchImpl {
         SArgs<T> a = make_args<T>(dsc, p, queries, cands, ws);
         const int dtype = EXACT ? TCDTW_F64 : TCDTW_F32;
         tm.mark(0);
+        if (p.f32f) {
+            if constexpr (!EXACT) {
+                // the float32 roundings the whole filter runs on (kept in the
+                // workspace for the finish phase) and the rounding slack
+                unsigned long long* mx = at<unsigned long long>(ws, p.o_slack) + 2;
+                cudaMemsetAsync(mx, 0, 16, st);
+                const int sms = sm_count();
+                round_points_kernel<<<sms * 8, 256, 0, st>>>((const double*)queries, p.Q * p.n, p.d,
+                                                            const_cast<T*>(a.queries), mx);
+                TRY(launch_status());
+                round_points_kernel<<<sms * 8, 256, 0, st>>>((const double*)cands, p.N * p.n, p.d,
+                                                            const_cast<T*>(a.cands), mx + 1);
+                TRY(launch_status());
+                f32_slack_kernel<<<1, 1, 0, st>>>(mx, p.n, at<float>(ws, p.o_slack));
+                TRY(launch_status());
+            }
+            queries = a.queries;
+            cands = a.cands;
+        }
         cudaMemsetAsync(at<char>(ws, p.o_ctr), 0, (size_t)p.Q * TCDTW_COUNTERS * 8, st);
         fill_kernel<T><<<grid_for(p.Q, 256), 256, 0, st>>>(a.dbest, p.Q, dev_inf<T>());
         TRY(launch_status());
@@ -3308,7 +3334,7 @@ struct SearchImpl {
                                 at<int32_t>(ws, p.o_bcnt), st));
         if (a.adv == TCDTW_METHOD_LB_TI && p.n > 1)
             TRY(series_steps(dtype, queries, p.Q, p.n, p.d, at<T>(ws, p.o_steps), st));
-        dbg_stage(st, "prep");
+        dbg_stage(dsc, st, "prep");
         tm.mark(1);
         if (p.has_lb)
             TRY((launch_lbmv_matrix<T, DMAX, EXACT>(at<T>(ws, p.o_upT), at<T>(ws, p.o_loT), at<T>(ws, p.o_qT),
@@ -3323,7 +3349,7 @@ struct SearchImpl {
                                                     at<T>(ws, p.o_qT), p.N, p.Q, p.n, p.d, at<T>(ws, p.o_lb2),
                                                     nullptr, st, 1, true)));
         }
-        dbg_stage(st, "lb_mv");
+        dbg_stage(dsc, st, "lb_mv");
         tm.mark(2);
         if (p.S > 0) {
             uint32_t* seeds = at<uint32_t>(ws, p.o_seed);
@@ -3343,13 +3369,14 @@ struct SearchImpl {
             TRY(launch_status());
             fill_kernel<T><<<grid_for(p.Q * p.S, 256), 256, 0, st>>>(at<T>(ws, p.o_seedres), p.Q * p.S, dev_inf<T>());
             TRY(launch_status());
-            dbg_stage(st, "topk+tiles");
+            dbg_stage(dsc, st, "topk+tiles");
             tm.mark(3);
-            TRY((launch_dtw<T, DMAX, EXACT>(a, p, stl, p.Q, seeds, at<T>(ws, p.o_seedres), at<int>(ws, p.o_tctr), st)));
+            TRY((launch_dtw<T, DMAX, EXACT>(a, p, stl, p.Q, seeds, at<T>(ws, p.o_seedres), at<int>(ws, p.o_tctr), st,
+                                            few_pairs(p.Q * (int64_t)p.S))));
         } else {
             tm.mark(3);
         }
-        dbg_stage(st, "seed dtw");
+        dbg_stage(dsc, st, "seed dtw");
         tm.mark(4);
         if (dbest_out && dbest_out != (void*)a.dbest)
             cudaMemcpyAsync(dbest_out, a.dbest, (size_t)p.Q * sizeof(T), cudaMemcpyDeviceToDevice, st);
@@ -3363,6 +3390,10 @@ struct SearchImpl {
         (void)dr;
         PhaseTimer tm(dsc, st, 4, 7);
         SArgs<T> a = make_args<T>(dsc, p, queries, cands, ws);
+        if (p.f32f) {  // the float32 copies the seed phase made
+            queries = a.queries;
+            cands = a.cands;
+        }
         const int sms = sm_count();
         tm.mark(4);
         if (dbest_in && dbest_in != (const void*)a.dbest)
@@ -3408,23 +3439,24 @@ struct SearchImpl {
         Tiles tl{at<uint32_t>(ws, p.o_tq), at<int64_t>(ws, p.o_tb), at<int32_t>(ws, p.o_tl)};
         seg_tiles_fill_kernel<<<grid_for(n_seg, 128), 128, 0, st>>>(p.Q, p.n_chunks, coff, toff, tl);
         TRY(launch_status());
-        // the number of tiles stays on the device: kernels stop at the first
-        // tile past the end (tile_q sentinel), bounded by max_tiles.
-        dbg_stage(st, "compact+tiles");
-        int64_t n_tiles = 0;
-        cudaMemcpyAsync(&n_tiles, toff + n_seg, 8, cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
+        // The number of tiles stays on the device (toff[n_seg], read by the
+        // kernels through tl.count); the host only knows the upper bound
+        // max_tiles, which sizes the grids.  No host synchronisation.
+        dbg_stage(dsc, st, "compact+tiles");
+        tl.count = toff + n_seg;
+        const int64_t n_tiles = p.max_tiles;
+        const bool survivors_few = few_pairs(p.Q * p.N);  // upper bound: every pair survives
         tm.mark(5);
-        if (a.adv >= 0 && n_tiles > 0) {
+        if (a.adv >= 0) {
             int sa = TCDTW_NOT_SUPPORTED;
-            if (a.adv == TCDTW_METHOD_LB_PC && !getenv("TCDTW_NO_PC_SMEM"))
+            if (a.adv == TCDTW_METHOD_LB_PC)
                 sa = launch_advanced_pc<T>(a, p.d, tl, n_tiles, surv, res, at<int>(ws, p.o_tctr), st);
             if (sa == TCDTW_NOT_SUPPORTED) {
                 cudaMemsetAsync(at<int>(ws, p.o_tctr), 0, sizeof(int), st);
                 int grid = (p.adv_warps * 32) / 256;
                 // LB_TI: slot rings in shared memory when 8 warps' rings fit
                 const size_t ring = (size_t)8 * 3 * p.B * 32 * sizeof(T);
-                bool rs = a.adv == TCDTW_METHOD_LB_TI && ring <= 200 * 1024 && !getenv("TCDTW_TI_GLOBAL_RING");
+                bool rs = a.adv == TCDTW_METHOD_LB_TI && ring <= 200 * 1024;
                 auto kern = advanced_kernel<T, DMAX, EXACT>;
                 if (rs && ring > 48 * 1024 &&
                     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring) != cudaSuccess)
@@ -3435,34 +3467,27 @@ struct SearchImpl {
             }
             TRY(sa);
         }
-        dbg_stage(st, "advanced");
+        dbg_stage(dsc, st, "advanced");
         if constexpr (!EXACT) {
             // the R-row lane kernel keeps one query per warp: hand it whole
             // segments, or, when segments are too few to occupy every warp
             // (small collections: C1 has 3 chunks per query), pieces of about
-            // survivors / (4 x resident warps), at least 4 pairs per lane
-            if (n_tiles > 0 && laner_rows(a, p.d, p.B) > 0 && !few_pairs(n_tiles * (int64_t)kTile)) {
-                const int64_t surv_est = n_tiles * (int64_t)kTile;
-                const int64_t warps = (int64_t)sms * 16;
-                int seg_len = (int)kChunk;
-                if (n_tiles * (int64_t)kTile / kChunk < 4 * warps) {
-                    int64_t want = surv_est / (4 * warps);
-                    seg_len = 128;
-                    while (seg_len < want && seg_len < (int)kChunk) seg_len <<= 1;
-                }
-                if (const char* sl = getenv("TCDTW_SEG_LEN")) seg_len = atoi(sl);
+            // survivors / (4 x resident warps), at least 4 pairs per lane --
+            // the piece length is chosen on the device from the tile count
+            if (laner_rows(a, p.d, p.B) > 0 && !survivors_few) {
+                int* seg_len = at<int>(ws, p.o_tctr) + 8;
+                laner_seglen_kernel<<<1, 1, 0, st>>>(tl.count, (int64_t)sms * 16, seg_len);
+                TRY(launch_status());
                 seg_tiles_count_kernel<<<grid_for(n_seg, 256), 256, 0, st>>>(p.Q, p.n_chunks, coff, tcnt, nullptr,
-                                                                             seg_len);
+                                                                             kChunk, seg_len);
                 TRY(launch_status());
                 cb = p.cub_bytes;
                 if (cub::DeviceScan::ExclusiveSum(at<void>(ws, p.o_cub), cb, tcnt, toff, (int)(n_seg + 1), st) !=
                     cudaSuccess)
                     return TCDTW_CUDA_ERROR;
-                seg_tiles_fill_kernel<<<grid_for(n_seg, 128), 128, 0, st>>>(p.Q, p.n_chunks, coff, toff, tl,
+                seg_tiles_fill_kernel<<<grid_for(n_seg, 128), 128, 0, st>>>(p.Q, p.n_chunks, coff, toff, tl, kChunk,
                                                                             seg_len);
                 TRY(launch_status());
-                cudaMemcpyAsync(&n_tiles, toff + n_seg, 8, cudaMemcpyDeviceToHost, st);
-                cudaStreamSynchronize(st);
             }
         }
         tm.mark(6);
@@ -3473,8 +3498,8 @@ struct SearchImpl {
         ad.done_list = done_list;
         ad.done_cnt = done_cnt;
         ad.done_cap = p.done_cap;
-        TRY((launch_dtw<T, DMAX, EXACT>(ad, p, tl, n_tiles, surv, res, at<int>(ws, p.o_tctr), st)));
-        dbg_stage(st, "dtw");
+        TRY((launch_dtw<T, DMAX, EXACT>(ad, p, tl, n_tiles, surv, res, at<int>(ws, p.o_tctr), st, survivors_few)));
+        dbg_stage(dsc, st, "dtw");
         tm.mark(7);
         // finalize
         T* minv = at<T>(ws, p.o_minv);
@@ -3492,7 +3517,7 @@ struct SearchImpl {
             fin_min_kernel<T><<<fgrid, 256, 0, st>>>(stl, p.Q, seedres, minv, nullptr, 0);
             TRY(launch_status());
         }
-        if (n_tiles > 0) {
+        {
             // completed survivors from the list; the full tile scan only if
             // the list overflowed (both decided on the device)
             fin_min_list_kernel<T><<<fgrid, 256, 0, st>>>(done_list, done_cnt, p.done_cap, res, minv);
@@ -3510,28 +3535,34 @@ struct SearchImpl {
         F.d64 = reinterpret_cast<double*>(F.item + p.fin_cap);
         F.cap = p.fin_cap;
         cudaMemsetAsync(F.cnt, 0, 8, st);
-        fin_collect_kernel<T><<<fgrid, 256, 0, st>>>(a, stl, p.S > 0 ? p.Q : 0, seeds, seedres,
-                                                     n_tiles > 0 ? done_list : nullptr, done_cnt, p.done_cap, surv,
-                                                     res, minv, dbi, F);
+        fin_collect_kernel<T><<<fgrid, 256, 0, st>>>(a, stl, p.S > 0 ? p.Q : 0, seeds, seedres, done_list, done_cnt,
+                                                     p.done_cap, surv, res, minv, dbi, F);
         TRY(launch_status());
         {
-            const size_t fsm = (size_t)8 * (2 * p.w + 1) * sizeof(double);  // one float64 band row per warp
-            if (fsm > 48 * 1024 &&
-                cudaFuncSetAttribute(fin_rescore_warp_kernel<T, DMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)fsm) != cudaSuccess)
-                return TCDTW_NOT_SUPPORTED;
-            fin_rescore_warp_kernel<T, DMAX><<<sms * 4, 256, fsm, st>>>(a, F, min64);
-            TRY(launch_status());
+            // per warp: the staged query (float64) and one band row (+inf end)
+            const size_t row_b = (size_t)(2 * p.w + 2) * sizeof(double);
+            const size_t stage_b = (size_t)p.n * rescore_col_stride(p.d) * sizeof(double) + row_b;
+            const int wpb = (int)(200 * 1024 / stage_b) < 8 ? (int)(200 * 1024 / stage_b) : 8;
+            auto go = [&](auto kern, int warps, size_t per_warp) -> int {
+                const size_t fsm = (size_t)warps * per_warp;
+                if (fsm > 48 * 1024 &&
+                    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm) != cudaSuccess)
+                    return TCDTW_NOT_SUPPORTED;
+                int occ = 1;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, fsm);
+                kern<<<sms * (occ < 1 ? 1 : occ), warps * 32, fsm, st>>>(a, F, min64);
+                return launch_status();
+            };
+            if (wpb >= 1) TRY(go(fin_rescore_warp_kernel<T, DMAX, true>, wpb, stage_b));
+            else TRY(go(fin_rescore_warp_kernel<T, DMAX, false>, 8, row_b));
         }
         // survivors' completed list overflowed: scan every tile instead
-        if (n_tiles > 0) {
-            fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, tl, n_tiles, surv, res, minv, dbi, EXACT ? 1 : 0,
-                                                               min64, bidx, fsc, done_cnt, p.done_cap);
-            TRY(launch_status());
-        }
+        fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, tl, n_tiles, surv, res, minv, dbi, EXACT ? 1 : 0,
+                                                           min64, bidx, fsc, done_cnt, p.done_cap);
+        TRY(launch_status());
         fin_pick_kernel<<<fgrid, 256, 0, st>>>(F, min64, bidx);
         TRY(launch_status());
-        if (n_tiles > 0 && !EXACT) {
+        if (!EXACT) {
             fin_rescore_kernel<T, DMAX><<<rgrid, 256, 0, st>>>(a, tl, n_tiles, surv, res, minv, dbi, 1, min64, bidx,
                                                                fsc, done_cnt, p.done_cap);
             TRY(launch_status());
@@ -3539,7 +3570,7 @@ struct SearchImpl {
         fin_output_kernel<T><<<grid_for(p.Q, 256), 256, 0, st>>>(p.Q, p.N, dsc->candidate_base, minv, min64, bidx,
                                                                 a.counters, p.has_lb ? 1 : 0, best_index,
                                                                 best_distance, counters);
-        dbg_stage(st, "finalize");
+        dbg_stage(dsc, st, "finalize");
         tm.mark(8 > TCDTW_PHASES ? TCDTW_PHASES : 8);
         tm.finish();
         return launch_status();

@@ -70,7 +70,9 @@ class ShardedSearch:
     def __init__(self, shard_candidates, base: int, n_total: int, dtype=None, group=None):
         from .search import SearchIndex
 
-        self.index = SearchIndex(shard_candidates, dtype=dtype, base=base)
+        # exact kernels for float64 shards: the float32 filter's rounding slack is
+        # per shard, which a cross-shard d_best exchange would not cover
+        self.index = SearchIndex(shard_candidates, dtype=dtype, base=base, f32_filter=False)
         self.n_total = int(n_total)
         self.group = group
 

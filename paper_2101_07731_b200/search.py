@@ -123,12 +123,20 @@ def _stack(candidates) -> np.ndarray:
 class SearchIndex:
     """A candidate collection (or one shard of it) resident on the GPU.
 
-    dtype "f64" runs the EXACT float64 path; "f32" stores float32 and runs
-    the float32 filter with float64 finalist re-scoring.  `base` is the
-    global index of candidate 0 (sharding).
+    dtype "f32" stores float32 and runs the float32 filter with float64
+    finalist re-scoring (on the float32 values).  dtype "f64" stores float64;
+    with ``f32_filter`` (the default when every value fits float32 comfortably)
+    the bounds and the DTW filter still run in float32, on a rounded copy the
+    library makes per call, with a slack covering the rounding, and the
+    finalists are re-scored in float64 on the original values -- the answers
+    and distances are the EXACT path's, bit for bit (TCDTW_FLAG_F32_FILTER);
+    ``f32_filter=False`` runs every kernel in float64.  `base` is the global
+    index of candidate 0 (sharding).
     """
 
-    def __init__(self, candidates, dtype=None, base: int = 0, device=None):
+    F32_FILTER_MAX_ABS = 1e30  # float32 copies must stay finite with room to spare
+
+    def __init__(self, candidates, dtype=None, base: int = 0, device=None, f32_filter: bool | None = None):
         t = _dev.torch()
         arr = _stack(candidates)
         if dtype is None:
@@ -144,7 +152,15 @@ class SearchIndex:
         if dev.ndim != 3 or dev.shape[0] < 1:
             raise InvalidInputError("candidate list is empty")
         self.candidates = dev.contiguous()
+        if not bool(t.isfinite(self.candidates).all()):
+            raise InvalidInputError("series contains non-finite values")
+        if self.dtype == "f64":
+            fits = float(self.candidates.abs().max()) < self.F32_FILTER_MAX_ABS
+            self.f32_filter = fits if f32_filter is None else (bool(f32_filter) and fits)
+        else:
+            self.f32_filter = False
         self.base = int(base)
+        self.done_cap = 0  # completed-DTW list capacity (0 = library default; tests force 1)
         self._ws = None
         self._ws_bytes = 0
         self._cenv = None  # (window, upper, lower): candidate-side index
@@ -174,12 +190,23 @@ class SearchIndex:
             self._cenv = (w, up, lo)
         return self._cenv[1], self._cenv[2]
 
+    def _filtering(self, reverse_bound: bool) -> bool:
+        return self.f32_filter and not reverse_bound
+
+    def work_tdtype(self, reverse_bound: bool = False):
+        """Element type of d_best and dim_range: float32 under the filter."""
+        t = _dev.torch()
+        return t.float32 if self._filtering(reverse_bound) else self.tdtype
+
     def _desc(self, params: SearchParams, adv: Method | None, n_q: int, seeds: int, timing: bool,
               phase_buf, reverse_bound: bool = False) -> _lib.SearchDesc:
         _, n, d = self.candidates.shape
         flags = _lib.FLAG_TIMING if timing else 0
+        rev = reverse_bound and params.method != Method.NONE
+        if self._filtering(rev):
+            flags |= _lib.FLAG_F32_FILTER
         cu = cl = None
-        if reverse_bound and params.method != Method.NONE:
+        if rev:
             cu, cl = self.candidate_envelopes(params.window)
             flags |= _lib.FLAG_REVERSE_LB
         return _lib.SearchDesc(
@@ -191,7 +218,7 @@ class SearchIndex:
             trigger_pc=params.trigger_pc, min_cell_frac=params.min_cell_frac, n_queries=n_q,
             n_candidates=self.n_candidates, candidate_base=self.base, seeds=seeds,
             flags=flags, phase_ms=ctypes.cast(phase_buf, ctypes.POINTER(ctypes.c_float)) if timing else None,
-            cand_upper=_lib.ptr(cu), cand_lower=_lib.ptr(cl))
+            cand_upper=_lib.ptr(cu), cand_lower=_lib.ptr(cl), done_cap=self.done_cap)
 
     def workspace_bytes(self, params: SearchParams, advanced=None, n_q: int = 1, seeds: int = 0,
                         reverse_bound: bool = False) -> int:
@@ -251,6 +278,8 @@ class SearchIndex:
             raise InvalidInputError(f"shape mismatch: {tuple(Q.shape[1:])} vs {tuple(self.candidates.shape[1:])}")
         if not bool(t.isfinite(Q).all()):
             raise InvalidInputError("series contains non-finite values")
+        if self.f32_filter and float(Q.abs().max()) >= self.F32_FILTER_MAX_ABS:
+            self.f32_filter = False  # queries outside the float32 comfort range: exact kernels
         return Q
 
     def seed_phase(self, qp, params: SearchParams, advanced=None, dim_range=None, seeds: int = 0,
@@ -266,10 +295,11 @@ class SearchIndex:
         L = _lib.lib()
         _lib.check(L.tcdtw_search_workspace_size(ctypes.byref(desc), ctypes.byref(nbytes)), "workspace_size")
         ws = self._workspace(int(nbytes.value))
+        wt = self.work_tdtype(reverse_bound)
         dr = None
         if dim_range is not None:
-            dr = _dev.to_dev(np.asarray(dim_range, dtype=np.float64).reshape(-1), self.tdtype)
-        dbest = t.empty(int(qp.shape[0]), dtype=self.tdtype, device=qp.device)
+            dr = _dev.to_dev(np.asarray(dim_range, dtype=np.float64).reshape(-1), wt)
+        dbest = t.empty(int(qp.shape[0]), dtype=wt, device=qp.device)
         _lib.check(L.tcdtw_search_seed(ctypes.byref(desc), qp.data_ptr(), self.candidates.data_ptr(), _lib.ptr(dr),
                                        ws.data_ptr(), ws.numel(), dbest.data_ptr(), _lib.stream_ptr()),
                    "search_seed")

@@ -1,0 +1,8 @@
+# round 2: C3 float32 filter + pipelined float64 re-score; ncu of the C3 DTW kernel
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "c3 or c0 or filter or edge or long" > gpurun_out/r2c3_tests.log 2>&1; echo "exit=$?" >> gpurun_out/r2c3_tests.log
+timeout 300 python bench.py --config C3 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/r2c3_c3.log 2>&1
+timeout 300 python bench.py --config C0 --steps 200 --warmup 5 --no-cpu-baseline > gpurun_out/r2c3_c0.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"dtw_wave_d|fin_rescore_warp" -s 2 -c 2 -o gpurun_out/r2c3_ncu python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/r2c3_ncu.log 2>&1
+echo "ncu exit=$?" >> gpurun_out/r2c3_ncu.log

@@ -178,16 +178,25 @@ def test_c0_all_methods_golden(P):
         assert np.all(c["dtw_computed"] + c["dtw_skipped"] == len(wl.candidates))
 
 
-def _oracle_check(P, cfg, wi, n_queries, method="lb_mv", advanced=None, dtype=None, rel=0.0):
+def _oracle_check(P, cfg, wi, n_queries, method="lb_mv", advanced=None, dtype=None, rel=0.0, f32_filter=None,
+                  spread=False):
+    """n_queries of the config against the oracle; ``spread`` samples seeded
+    random query indices across the whole query set instead of the first."""
     from oracle import oracle as O
     from paper_2101_07731_b200.datasets import make_workload
 
     wl = make_workload(cfg)
     w = wl.spec.windows()[wi]
-    qsel = wl.queries[:n_queries]
-    res = P.SearchIndex(wl.candidates, dtype=dtype or wl.dtype).search(
-        qsel, _params(P, w, method), advanced=None if advanced is None else P.Method(advanced),
-        dim_range=wl.dim_range)
+    if spread:
+        pick = np.sort(np.random.default_rng(99).choice(len(wl.queries), size=n_queries, replace=False))
+        qsel = wl.queries[pick]
+    else:
+        qsel = wl.queries[:n_queries]
+    index = P.SearchIndex(wl.candidates, dtype=dtype or wl.dtype, f32_filter=f32_filter)
+    if f32_filter is not None:
+        assert index.f32_filter == (f32_filter and index.dtype == "f64")
+    res = index.search(qsel, _params(P, w, method), advanced=None if advanced is None else P.Method(advanced),
+                       dim_range=wl.dim_range)
     outs, _ = O.nn_search_batch(qsel.astype(np.float64), wl.candidates.astype(np.float64),
                                 O.make_params(w, method), advanced, wl.dim_range)
     for i, o in enumerate(outs):
@@ -218,11 +227,41 @@ def test_c2_parity(P):
 
 
 def test_c3_parity(P):
-    _oracle_check(P, "C3", 0, 24, rel=0.0)
+    # float64 data: the float32 filter + float64 re-score on the originals
+    # (the default) and the all-float64 kernels give the reference's bits
+    _oracle_check(P, "C3", 0, 24, rel=0.0, f32_filter=True)
+    _oracle_check(P, "C3", 0, 8, rel=0.0, f32_filter=False)
+
+
+def test_c0_filter_and_exact_paths(P):
+    for flt in (True, False):
+        for method, adv in (("lb_mv", None), ("lb_pc", None), ("tc_dtw", "lb_ti"), ("none", None)):
+            _oracle_check(P, "C0", 0, 20, method=method, advanced=adv, rel=0.0, f32_filter=flt)
 
 
 def test_c4_sampled_parity(P):
-    _oracle_check(P, "C4", 0, 16, rel=0.0)
+    # spread-out query indices: fp32 near-ties are likeliest at C4
+    _oracle_check(P, "C4", 0, 24, rel=0.0, spread=True)
+
+
+@pytest.mark.parametrize("n,d,w", [(64, 3, 6), (200, 5, 20), (300, 8, 60), (129, 1, 0), (40, 20, 4), (512, 6, 51)])
+def test_f32_filter_matches_exact_kernels(P, rng, n, d, w):
+    """float64 inputs: the float32-filtered search returns the all-float64
+    search's indices and distances bit for bit, including exact ties,
+    near-ties below float32 resolution and a wide value range."""
+    cands = np.cumsum(rng.normal(size=(300, n, d)), axis=1) * 10.0 ** rng.uniform(-3, 3)
+    queries = cands[:12] + rng.normal(size=(12, n, d)) * 1e-9  # near-ties far below float32 resolution
+    queries[3] = cands[40]  # exact match
+    cands[41] = cands[40]  # exact tie: the lower index wins
+    out = {}
+    for flt in (True, False):
+        idx = P.SearchIndex(cands, dtype="f64", f32_filter=flt)
+        assert idx.f32_filter == flt
+        res = idx.search(queries, _params(P, w, "lb_mv"))
+        out[flt] = (res.best_index, res.best_distance)
+    assert np.array_equal(out[True][0], out[False][0])
+    assert np.array_equal(out[True][1], out[False][1])
+    assert out[True][0][3] == 40 and out[True][1][3] == 0.0
 
 
 # ------------------------------------------------------------- edge cases
@@ -302,30 +341,38 @@ def test_sharded_combine_equals_single(P):
 
 def test_completed_list_overflow_path(P, monkeypatch):
     """Finalisation normally visits only the list of completed DTWs; with a
-    capacity of 1 it must fall back to scanning every survivor tile and still
-    return the same answers."""
-    monkeypatch.setenv("TCDTW_DONE_CAP", "1")
+    capacity of 1 (tcdtw_search_desc.done_cap) it must fall back to scanning
+    every survivor tile and still return the same answers."""
+    orig = P.SearchIndex.__init__
+
+    def tiny_list(self, *a, **k):
+        orig(self, *a, **k)
+        self.done_cap = 1
+
+    monkeypatch.setattr(P.SearchIndex, "__init__", tiny_list)
     _oracle_check(P, "C1", 0, 24, rel=0.0)
-    _oracle_check(P, "C0", 0, 20, rel=0.0)
+    _oracle_check(P, "C0", 0, 20, rel=0.0, f32_filter=True)
+    _oracle_check(P, "C0", 0, 20, rel=0.0, f32_filter=False)
 
 
 @pytest.mark.parametrize("dt,n,d,w", [("f32", 256, 5, 51), ("f64", 256, 5, 51), ("f64", 256, 8, 51),
                                       ("f32", 1024, 8, 102), ("f64", 512, 8, 102), ("f64", 1024, 8, 40),
                                       ("f32", 200, 3, 70), ("f64", 97, 2, 33)])
-@pytest.mark.parametrize("pipe", [False, True])
-def test_long_band_shapes(P, dt, n, d, w, pipe, monkeypatch):
-    """Long bands (2W+1 > 64): wavefront kernels (and the opt-in row pipeline); ragged n (not
-    a multiple of 32) and rows near the end of the band are the edge cases."""
+@pytest.mark.parametrize("f32_filter", [True, False])
+def test_long_band_shapes(P, dt, n, d, w, f32_filter):
+    """Long bands (2W+1 > 64): wavefront kernels; ragged n (not a multiple of
+    32) and rows near the end of the band are the edge cases; float64 data
+    through the float32 filter and through the float64 kernels."""
     from oracle import oracle as O
 
-    if pipe:
-        monkeypatch.setenv("TCDTW_PIPE", "1")
+    if dt == "f32" and not f32_filter:
+        pytest.skip("float32 data always filters in float32")
     rng = np.random.default_rng(n * 100 + w)
     C = np.cumsum(rng.normal(size=(40, n, d)), axis=1)
     Qs = np.cumsum(rng.normal(size=(3, n, d)), axis=1)
     if dt == "f32":
         C, Qs = C.astype(np.float32), Qs.astype(np.float32)
-    res = P.SearchIndex(C, dtype=dt).search(Qs, P.SearchParams(window=w, method="lb_mv"))
+    res = P.SearchIndex(C, dtype=dt, f32_filter=f32_filter).search(Qs, P.SearchParams(window=w, method="lb_mv"))
     outs, _ = O.nn_search_batch(Qs.astype(np.float64), C.astype(np.float64), O.make_params(w, "lb_mv"), None, None)
     assert res.best_index.tolist() == [o.best_index for o in outs]
     assert res.best_distance.tolist() == [o.best_distance for o in outs]

@@ -1,5 +1,7 @@
-"""Config-level parity evidence: every query of C0-C3 (C1 at both windows)
-and a 64-query C4 sample searched on the GPU and by the C oracle, compared
+"""Config-level parity evidence: every query of C0-C3 (C1 at both windows;
+the float64 configs through both the float32 filter and the all-float64
+kernels) and 256 seeded random C4 queries (spread over all 10,000) searched
+on the GPU and by the C oracle, compared
 index for index and distance for distance (==).  A few minutes of oracle
 work, so it only runs with TCDTW_FULL_PARITY=1:
 
@@ -23,15 +25,19 @@ def test_full_parity():
     from oracle import oracle as O
     from paper_2101_07731_b200.datasets import make_workload
 
-    runs = [("C0", 0, None, "lb_mv"), ("C0", 0, None, "lb_pc"), ("C1", 0, None, "lb_mv"), ("C1", 1, None, "lb_mv"),
-            ("C2", 0, None, "lb_mv"), ("C3", 0, None, "lb_mv"), ("C4", 0, 64, "lb_mv")]
+    runs = [("C0", 0, None, "lb_mv", True), ("C0", 0, None, "lb_pc", True), ("C0", 0, None, "lb_mv", False),
+            ("C1", 0, None, "lb_mv", None), ("C1", 1, None, "lb_mv", None), ("C2", 0, None, "lb_mv", None),
+            ("C3", 0, None, "lb_mv", True), ("C3", 0, None, "lb_mv", False), ("C4", 0, 256, "lb_mv", None)]
     all_ok = True
-    for cfg, wi, nq, method in runs:
+    for cfg, wi, nq, method, flt in runs:
         wl = make_workload(cfg)
         w = wl.spec.windows()[wi]
-        qs = wl.queries if nq is None else wl.queries[:nq]
+        if nq is None:
+            qs = wl.queries
+        else:
+            qs = wl.queries[np.sort(np.random.default_rng(7).choice(len(wl.queries), size=nq, replace=False))]
         t0 = time.perf_counter()
-        res = P.SearchIndex(wl.candidates, dtype=wl.dtype).search(
+        res = P.SearchIndex(wl.candidates, dtype=wl.dtype, f32_filter=flt).search(
             qs, P.SearchParams(window=w, method=P.Method(method)), dim_range=wl.dim_range)
         t_gpu = time.perf_counter() - t0
         t0 = time.perf_counter()
@@ -45,7 +51,8 @@ def test_full_parity():
         rel = float(np.max(np.abs(res.best_distance - od) / np.maximum(od, 1e-300)))
         ok = same_i == len(qs) and same_d == len(qs)
         all_ok &= ok
-        print(f"{cfg} W={w} {method} {wl.dtype}: {len(qs)} queries x {len(wl.candidates)} candidates; "
+        mode = {True: " f32-filter", False: " exact-f64", None: ""}[flt]
+        print(f"{cfg} W={w} {method} {wl.dtype}{mode}: {len(qs)} queries x {len(wl.candidates)} candidates; "
               f"indices equal {same_i}/{len(qs)}, distances equal (==) {same_d}/{len(qs)}, max rel diff {rel:.3g}; "
               f"GPU {t_gpu:.2f} s (incl. upload), oracle {t_cpu:.1f} s on {used} threads -> {'OK' if ok else 'MISMATCH'}",
               flush=True)

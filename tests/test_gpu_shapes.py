@@ -16,7 +16,7 @@ SHAPES = [  # (n, d, W)
 
 
 @pytest.mark.parametrize("n,d,w", SHAPES)
-@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("dtype", ["f32", "f64", "f64-exact"])
 def test_search_shapes(n, d, w, dtype):
     import paper_2101_07731_b200 as P
     from oracle import oracle as O
@@ -28,7 +28,9 @@ def test_search_shapes(n, d, w, dtype):
     np_t = np.float32 if dtype == "f32" else np.float64
     X = X.astype(np_t)
     cands, qs = X[:N], X[N:]
-    res = P.SearchIndex(cands, dtype=dtype).search(qs, P.SearchParams(window=w, method=P.Method.LB_MV))
+    # f64: the float32 filter on float64 data (default); f64-exact: every kernel in float64
+    index = P.SearchIndex(cands, dtype=dtype[:3], f32_filter=None if dtype != "f64-exact" else False)
+    res = index.search(qs, P.SearchParams(window=w, method=P.Method.LB_MV))
     outs, _ = O.nn_search_batch(qs.astype(np.float64), cands.astype(np.float64), O.make_params(w, "lb_mv"), None,
                                 None)
     for i, o in enumerate(outs):
@@ -38,7 +40,8 @@ def test_search_shapes(n, d, w, dtype):
     assert np.all(c["dtw_computed"] + c["dtw_skipped"] == N)
 
 
-@pytest.mark.parametrize("n,d,w,dtype", [(4096, 8, 409, "f64"), (4096, 6, 409, "f32"), (2048, 3, 1000, "f64")])
+@pytest.mark.parametrize("n,d,w,dtype", [(4096, 8, 409, "f64"), (4096, 8, 409, "f64-exact"), (4096, 6, 409, "f32"),
+                                          (2048, 3, 1000, "f64"), (2048, 3, 1000, "f64-exact")])
 def test_long_series(n, d, w, dtype):
     """Series whose staged query rows exceed shared memory: the wavefront
     reads them through L1; wide bands: the float64 re-score's band rows."""
@@ -49,7 +52,8 @@ def test_long_series(n, d, w, dtype):
     N, Q = 40, 2
     X = np.cumsum(rng.normal(size=(N + Q, n, d)), axis=1)
     X = ((X - X.reshape(-1, d).mean(0)) / X.reshape(-1, d).std(0)).astype(np.float32 if dtype == "f32" else np.float64)
-    res = P.SearchIndex(X[:N], dtype=dtype).search(X[N:], P.SearchParams(window=w, method=P.Method.LB_MV))
+    index = P.SearchIndex(X[:N], dtype=dtype[:3], f32_filter=None if dtype != "f64-exact" else False)
+    res = index.search(X[N:], P.SearchParams(window=w, method=P.Method.LB_MV))
     outs, _ = O.nn_search_batch(X[N:].astype(np.float64), X[:N].astype(np.float64), O.make_params(w, "lb_mv"),
                                 None, None)
     assert list(res.best_index) == [o.best_index for o in outs]
