@@ -314,6 +314,10 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        if args.dist_backend == "nccl":  # the init log lets the driver verify the rank count
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+
         dev = local if args.dist_backend == "nccl" else local % torch.cuda.device_count()
         torch.cuda.set_device(dev)
         if args.dist_backend == "nccl":

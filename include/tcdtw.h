@@ -221,6 +221,15 @@ int tcdtw_nn_search(const tcdtw_search_desc *desc, const void *queries, const vo
                     const void *dim_range, void *workspace, size_t ws_bytes, int64_t *best_index,
                     double *best_distance, int64_t *counters, void *stream);
 
+/* Cross-shard combine (no reference counterpart -- the
+ * reference is single-process).  records (world, n_queries, 2)
+ * int64 on the device: every rank's (float64 best_distance bits, global
+ * best_index) as gathered by one all-gather; writes the lexicographic
+ * (distance, index) minimum per query -- lowest index on equal distances,
+ * search.py:173 -- ignoring index -1 entries. */
+int tcdtw_shard_combine(const int64_t *records, int32_t world, int64_t n_queries, int64_t *best_index,
+                        double *best_distance, void *stream);
+
 /* Standalone LB_MV matrix (the search's dominant streaming kernel), for
  * benchmarking: out (n_queries, n_candidates) = LB_MV of every pair given
  * query envelopes (n_queries, n, dims). */

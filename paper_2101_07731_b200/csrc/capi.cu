@@ -36,6 +36,7 @@ int alu_probe(int, int, int, void*, double*, cudaStream_t);
 const char* dtw_kernel_name(const tcdtw_search_desc*);
 size_t normalize_workspace_bytes(int64_t, int);
 int normalize_f64(const double*, int64_t, int, double*, double*, double*, double*, double*, cudaStream_t);
+int shard_combine(const int64_t*, int, int64_t, int64_t*, double*, cudaStream_t);
 }  // namespace tcdtw
 
 using namespace tcdtw;
@@ -205,5 +206,11 @@ int tcdtw_normalize(const double* values, int64_t n_points, int32_t dims, double
     if (!values || !out || !mean || !std_ || !range) return TCDTW_INVALID_INPUT;
     if (!workspace || ws_bytes < normalize_workspace_bytes(n_points, dims)) return TCDTW_WORKSPACE_TOO_SMALL;
     return normalize_f64(values, n_points, dims, out, mean, std_, range, (double*)workspace, S(stream));
+}
+int tcdtw_shard_combine(const int64_t* records, int32_t world, int64_t n_queries, int64_t* best_index,
+                        double* best_distance, void* stream) {
+    if (world < 1 || n_queries < 0 || (n_queries > 0 && (!records || !best_index || !best_distance)))
+        return TCDTW_INVALID_INPUT;
+    return shard_combine(records, world, n_queries, best_index, best_distance, S(stream));
 }
 }  // extern "C"

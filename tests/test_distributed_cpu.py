@@ -1,8 +1,11 @@
 """World-size-2 gloo tests of the sharded-search collectives (CPU tensors).
 
 The NCCL path on the GPUs runs the same functions; here each rank holds a
-fake per-shard result and the lexicographic (distance, index) combination,
-the d_best exchange and the counter sum are checked against a host merge."""
+fake per-shard result: the one all-gather of (distance bits, index) records
+(its layout, world x Q x 2), the d_best exchange and the counter sum are
+checked against a host merge.  The reduction of the gathered records is
+the library's CUDA kernel (tcdtw_shard_combine), checked on the GPU
+(tests/test_gpu_sharded.py)."""
 
 import os
 import socket
@@ -27,7 +30,7 @@ def _worker(rank, world, port, q):
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        from paper_2101_07731_b200.distributed import combine_results, exchange_dbest, shard_bounds, sum_counters
+        from paper_2101_07731_b200.distributed import exchange_dbest, gather_records, shard_bounds, sum_counters
 
         rng = np.random.default_rng(7)
         n_q = 64
@@ -40,12 +43,10 @@ def _worker(rank, world, port, q):
         dists[1, ::5] = np.inf
         my_idx = torch.tensor(idx[rank], dtype=torch.int64)
         my_d = torch.tensor(dists[rank], dtype=torch.float64)
-        gi, gd = combine_results(my_idx, my_d)
-        # host merge: lexicographic (distance, index) over ranks
-        exp_d = dists.min(axis=0)
-        exp_i = np.array([min(idx[r, k] for r in range(world) if dists[r, k] == exp_d[k] and idx[r, k] >= 0)
-                          for k in range(n_q)])
-        ok = bool(np.array_equal(gd.numpy(), exp_d) and np.array_equal(gi.numpy(), exp_i))
+        rec = gather_records(my_idx, my_d)  # the one combine collective
+        ok = tuple(rec.shape) == (world, n_q, 2)
+        ok &= bool(np.array_equal(rec[:, :, 1].numpy(), idx))
+        ok &= bool(np.array_equal(rec[:, :, 0].numpy().view(np.float64), dists))
         db = torch.tensor(dists[rank], dtype=torch.float32)
         exchange_dbest(db)
         ok &= bool(np.array_equal(db.numpy(), dists.min(axis=0).astype(np.float32)))

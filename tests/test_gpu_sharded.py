@@ -77,3 +77,27 @@ def test_sharded_search_two_ranks_gloo():
     assert [o.best_distance for o in outs] == d0.tolist()
     # counters summed over shards: computed + skipped = N
     assert np.all(c0[:, 0] + c0[:, 1] == len(wl.candidates))
+
+
+def test_shard_combine_kernel(rng):
+    """tcdtw_shard_combine on gathered records: lexicographic (distance,
+    index) minimum, index -1 never wins, ties across ranks -> lowest index."""
+    import torch
+
+    from paper_2101_07731_b200.distributed import combine_gathered
+
+    world, n_q = 5, 257
+    dists = np.round(rng.uniform(0, 4, (world, n_q)), 1)
+    dists[:, ::7] = 1.5
+    idx = rng.integers(0, 10_000, (world, n_q))
+    idx[1, ::5] = -1
+    dists[1, ::5] = np.inf
+    idx[:, 3] = -1  # no rank has a result
+    dists[:, 3] = np.inf
+    rec = np.stack([dists.view(np.int64), idx], axis=2)
+    gi, gd = combine_gathered(torch.from_numpy(rec).cuda())
+    gi, gd = gi.cpu().numpy(), gd.cpu().numpy()
+    for k in range(n_q):
+        cands = [(dists[r, k], idx[r, k]) for r in range(world) if idx[r, k] >= 0]
+        want = min(cands) if cands else (np.inf, -1)
+        assert gd[k] == want[0] and gi[k] == want[1], k
