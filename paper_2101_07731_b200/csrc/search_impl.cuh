@@ -711,6 +711,8 @@ struct SArgs {
     // on (queries / cands are then their float32 roundings); else nullptr
     const double* xq;
     const double* xc;
+    // R-row lane kernel: per-warp scratch of its head batches (nullptr: none)
+    float* lane_scratch;
 };
 
 template <typename T>
@@ -1465,6 +1467,12 @@ struct LaneRLayout {
     __host__ __device__ static int warp_words(int n, int qrows, int B) { return q_words(qrows) + e_words(n) + B * 32; }
 };
 
+// Per-warp global scratch of the lane kernel's head batches: the parked
+// body state (band rows + scalars) and the queued pairs' band rows,
+// lane-interleaved (coalesced).
+__host__ __device__ inline int laner_scratch_words(int B) { return 2 * B * 32 + 9 * 32; }
+constexpr int kLanerMaxWarps = 148 * 32;
+
 template <int D, int B, int R, bool CASC, int MINB>
 __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Tiles tl, int64_t n_tiles,
                                                              const uint32_t* __restrict__ cand_of,
@@ -1475,6 +1483,11 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     constexpr int NIT = B + R - 1;              // iterations per step
     constexpr int JF = (B - 1 - R) / R;         // full blocks j = 1..JF (all rows inside the band)
     constexpr int ST = R * (JF + 1);            // first tail iteration
+    // Head batches: the first HS steps of a pair (rows 0 .. R*HS-1) start at
+    // iteration s0 = W - i >= R (earlier columns are < 0), rounded down to a
+    // whole block (j0 = s0 / R).  A warp runs them in lockstep for up to 32
+    // fresh pairs, so the trimmed iterations are skipped by the whole warp.
+    constexpr int HS = (W >= R) ? W / R : 0;
     static_assert(B >= R + 1 && JF >= 1, "band too narrow for R rows per step");
     extern __shared__ __align__(16) float smem_f[];
     const int n = a.n;
@@ -1486,11 +1499,30 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     const unsigned FULL = 0xffffffffu;
     const float INF = dev_inf<float>();
     const bool casc = CASC && a.lb != nullptr && a.abandon && a.env_up != nullptr;
+    const bool heads = HS > 0 && n > R * (HS + 1) && a.lane_scratch != nullptr;
+    float* const scr = a.lane_scratch + (size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * laner_scratch_words(B);
+    float* const park_band = scr + lane;
+    float* const queue_band = scr + 32 * B;
+    int* const park_i = reinterpret_cast<int*>(scr + 64 * B);
+    int* const park_el = park_i + 32;
+    int* const park_eh = park_i + 64;
+    uint32_t* const park_c = reinterpret_cast<uint32_t*>(park_i + 96);
+    float* const park_lb = scr + 64 * B + 128;
+    float* const park_pre = scr + 64 * B + 160;
+    int* const park_busy = park_i + 192;
+    // queued pairs (slot = the head lane that ran them): band row, LB_MV
+    // total and cascade prefix in scratch; the candidate stays in that lane's
+    // register q_cand (the pop's row loads depend on it)
+    float* const q_lb = scr + 64 * B + 224;
     // warp-uniform work state: current tile, reservoir window, query in smem
     int64_t t_begin = 0;
     int t_q = -1, t_len = 0, t_next = 0, r_base = 0, slot_q = -1;
     bool exhausted = false, have_tile = false;
     float t_thr_raw = INF;
+    unsigned q_mask = 0;  // queued slots (their first R*HS rows done)
+    int64_t q_base = 0;   // entry of slot 0
+    uint32_t q_cand = 0;  // candidate of this lane's queued slot
+    int head_h = -1;      // >= 0: a head batch is running, at head step head_h
     // reservoir: lane m holds entry r_base + m of the tile
     uint32_t pf_c = 0;
     float pf_lb = 0.f, pf_res = 0.f;
@@ -1498,7 +1530,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     bool busy = false;
     int64_t ent = 0;
     int i = 0, since = 0;
-    const float* crow = nullptr;
+    uint32_t cand = 0;
     float c[RD], nc[RD];
     float thr = INF, thr_pend_raw = INF, lbtot = 0.f, prefix = 0.f;
     int cq = -1;
@@ -1513,8 +1545,8 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
         }
         c_comp = c_ab = c_cells = c_issued = 0;
     };
-    auto load_rows = [&](float (&dst)[RD], const float* cr, int row) {  // rows row..row+R-1, row % R == 0
-        const float4* src = reinterpret_cast<const float4*>(cr + (int64_t)row * D);
+    auto load_rows = [&](float (&dst)[RD], uint32_t cc, int row) {  // rows row..row+R-1, row % R == 0
+        const float4* src = reinterpret_cast<const float4*>(a.cands + ((int64_t)cc * n + row) * D);
 #pragma unroll
         for (int v = 0; v < RD / 4; ++v) {
             const float4 x = __ldg(src + v);
@@ -1553,32 +1585,110 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
         slot_q = q;
         __syncwarp();
     };
+    auto start_pair = [&](int64_t e, uint32_t cc, float lb) {  // row 0 of a fresh pair (band init)
+        if (t_q != cq) {
+            flush();
+            cq = t_q;
+        }
+        ent = e;
+        cand = cc;
+        lbtot = lb;
+        prefix = 0.f;
+        thr = a.abandon ? scale_up<float>(t_thr_raw, a.mg) : INF;
+        thr_pend_raw = t_thr_raw;
+#pragma unroll
+        for (int k = 0; k < B; ++k) ps[k * 32] = (k == W) ? 0.f : INF;
+        load_rows(c, cc, 0);
+        i = 0;
+        since = 0;
+        busy = true;
+    };
+    // next tile (warp-uniform); false when none is left
+    auto next_tile = [&]() -> bool {
+        int64_t tile = 0;
+        if (lane == 0) tile = atomicAdd(tile_ctr, 1);
+        tile = __shfl_sync(FULL, tile, 0);
+        if (tile >= n_tiles) {
+            exhausted = true;
+            return false;
+        }
+        t_q = (int)tl.q[tile];
+        t_begin = tl.begin[tile];
+        t_len = tl.len[tile];
+        t_next = 0;
+        r_base = 0;
+        have_tile = true;
+        load_reservoir();
+        return true;
+    };
+    // Body refill: free lanes take queued pairs; with the queue empty, either
+    // a head batch starts (heads) or fresh pairs start at row 0 (no heads).
     auto refill = [&]() {
         unsigned freem = __ballot_sync(FULL, !busy);
         if (__popc(freem) < a.refill_min && freem != FULL) return;
-        while (freem && !exhausted) {
+        while (freem) {
+            if (q_mask) {  // pop: the rank-th free lane takes the rank-th queued slot
+                const int take = min(__popc(q_mask), __popc(freem));
+                const int rank = __popc(freem & ((1u << lane) - 1u));
+                const int sl = (int)__fns(q_mask, 0, (rank < take ? rank : 0) + 1);
+                const uint32_t cs = __shfl_sync(FULL, q_cand, sl);
+                if (!busy && rank < take) {
+                    ent = q_base + sl;
+                    cand = cs;
+                    lbtot = q_lb[sl];
+                    prefix = q_lb[32 + sl];
+                    i = R * HS;
+                    load_rows(c, cand, i);
+#pragma unroll
+                    for (int k = 0; k < B; ++k) ps[k * 32] = queue_band[k * 32 + sl];
+                    const float raw = a.abandon ? load_volatile(a.dbest + slot_q) : INF;
+                    thr = a.abandon ? scale_up<float>(raw, a.mg) : INF;
+                    thr_pend_raw = raw;
+                    since = 0;
+                    busy = true;
+                }
+                for (int k = 0; k < take; ++k) q_mask &= q_mask - 1;  // the lowest `take` slots are gone
+                freem = __ballot_sync(FULL, !busy);
+                continue;
+            }
+            if (exhausted) return;
             if (!have_tile || t_next >= t_len) {
                 have_tile = false;
-                int64_t tile = 0;
-                if (lane == 0) tile = atomicAdd(tile_ctr, 1);
-                tile = __shfl_sync(FULL, tile, 0);
-                if (tile >= n_tiles) {
-                    exhausted = true;
-                    break;
-                }
-                t_q = (int)tl.q[tile];
-                t_begin = tl.begin[tile];
-                t_len = tl.len[tile];
-                t_next = 0;
-                r_base = 0;
-                have_tile = true;
-                load_reservoir();
+                if (!next_tile()) return;
             }
             if (t_q != slot_q) {
                 // the slot still serves busy lanes of the previous query: drain first
                 if (freem != FULL) return;
                 load_query(t_q);
             }
+            if (heads) {
+                // head batch: park the busy lanes, take the next (up to) 32
+                // entries of the tile -- the reservoir window, lane m <-> entry
+                // r_base + m (batches consume whole windows) -- one per lane
+                park_busy[lane] = busy ? 1 : 0;
+                if (busy) {
+                    park_i[lane] = i;
+                    park_el[lane] = (int)(uint32_t)ent;
+                    park_eh[lane] = (int)(ent >> 32);
+                    park_c[lane] = cand;
+                    park_lb[lane] = lbtot;
+                    park_pre[lane] = prefix;
+#pragma unroll
+                    for (int k = 0; k < B; ++k) park_band[k * 32] = ps[k * 32];
+                }
+                busy = false;
+                const int avail = min(t_len - t_next, 32);
+                q_base = t_begin + t_next;
+                if (lane < avail && !(pf_res < 0.f)) start_pair(q_base + lane, pf_c, pf_lb);
+                t_next += avail;
+                if (t_next < t_len) {
+                    r_base += 32;
+                    load_reservoir();
+                }
+                head_h = 0;
+                return;
+            }
+            // no head batches (short series / narrow band): start at row 0
             if (t_next >= r_base + 32) {
                 r_base += 32;
                 load_reservoir();
@@ -1590,27 +1700,43 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
             const uint32_t c_m = __shfl_sync(FULL, pf_c, m);
             const float lb_m = __shfl_sync(FULL, pf_lb, m);
             const float res_m = __shfl_sync(FULL, pf_res, m);
-            if (!busy && rank < take && !(res_m < 0.f)) {  // skip entries pruned by the advanced bound
-                if (t_q != cq) {
-                    flush();
-                    cq = t_q;
-                }
-                ent = t_begin + r_base + m;
-                crow = a.cands + (int64_t)c_m * n * D;
-                lbtot = lb_m;
-                prefix = 0.f;
-                thr = a.abandon ? scale_up<float>(t_thr_raw, a.mg) : INF;
-                thr_pend_raw = t_thr_raw;
-#pragma unroll
-                for (int k = 0; k < B; ++k) ps[k * 32] = (k == W) ? 0.f : INF;
-                load_rows(c, crow, 0);
-                i = 0;
-                since = 0;
-                busy = true;
-            }
+            if (!busy && rank < take && !(res_m < 0.f))  // skip entries pruned by the advanced bound
+                start_pair(t_begin + r_base + m, c_m, lb_m);
             t_next += take;
             freem = __ballot_sync(FULL, !busy);
         }
+    };
+    // The head batch is over: survivors join the queue (slot = their lane),
+    // parked lanes resume -- their next rows were prefetched into nc during
+    // the last head step.
+    auto end_heads = [&]() {
+        q_mask = __ballot_sync(FULL, busy);
+        if (busy) {
+            q_cand = cand;
+            q_lb[lane] = lbtot;
+            q_lb[32 + lane] = prefix;
+#pragma unroll
+            for (int k = 0; k < B; ++k) queue_band[k * 32 + lane] = ps[k * 32];
+        }
+        __syncwarp();
+        busy = park_busy[lane] != 0;
+        if (busy) {
+            i = park_i[lane];
+            ent = (int64_t)(uint32_t)park_el[lane] | ((int64_t)park_eh[lane] << 32);
+            cand = park_c[lane];
+            lbtot = park_lb[lane];
+            prefix = park_pre[lane];
+#pragma unroll
+            for (int k = 0; k < B; ++k) ps[k * 32] = park_band[k * 32];
+            const float raw = a.abandon ? load_volatile(a.dbest + slot_q) : INF;
+            thr = a.abandon ? scale_up<float>(raw, a.mg) : INF;
+            thr_pend_raw = raw;
+#pragma unroll
+            for (int u = 0; u < RD; ++u) c[u] = nc[u];
+            since = 0;
+        }
+        __syncwarp();
+        head_h = -1;
     };
     float cur[R], prv[R], pu = 0.f, rmin = INF;
     // iteration s of the step: window column i - W + s for rows i..i+R-1.
@@ -1660,22 +1786,33 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
         }
     };
     while (true) {
-        refill();
-        if (!__any_sync(FULL, busy) && exhausted) break;
-        c_issued += R * B;
+        if (head_h < 0) {
+            refill();
+            if (!__any_sync(FULL, busy) && exhausted && q_mask == 0) break;
+        }
+        // head step h: rows i = R h .. with the first (W - i) / R blocks
+        // skipped (their columns are < 0); body steps start at block 0
+        const int j0 = head_h >= 0 ? (W - R * head_h) / R : 0;
+        c_issued += head_h >= 0 ? R * (B - R * j0) + R * (R - 1) / 2 : R * B;
         if (c_cells >= (1u << 30) || c_issued >= (1u << 30)) flush();
+        const bool last_head = head_h == HS - 1;
+        if (last_head && park_busy[lane]) load_rows(nc, park_c[lane], park_i[lane]);  // the parked pair's rows
         if (busy) {
             const bool more = i + R < n;
-            if (more) load_rows(nc, crow, i + R);  // consumed after the DP
+            if (more && !last_head) load_rows(nc, cand, i + R);  // consumed after the DP
 #pragma unroll
             for (int r = 0; r < R; ++r) cur[r] = prv[r] = INF;
             rmin = INF;
-            pu = ps[0];
             const float* qg = qs + (i / R) * QGS;  // padded column i + s <-> query column i - W + s
+            if (j0 == 0) {
+                pu = ps[0];
 #pragma unroll
-            for (int s = 0; s < R; ++s) iter(s, false, qg + s * 2 * DP, ps + s * 32);
+                for (int s = 0; s < R; ++s) iter(s, false, qg + s * 2 * DP, ps + s * 32);
+            } else {
+                pu = ps[j0 * R * 32];
+            }
 #pragma unroll 1
-            for (int j = 1; j <= JF; ++j) {
+            for (int j = j0 > 1 ? j0 : 1; j <= JF; ++j) {
                 const float* qb = qg + j * QGS;
                 float* pb = ps + j * R * 32;
 #pragma unroll
@@ -1739,6 +1876,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                 }
             }
         }
+        if (head_h >= 0 && ++head_h == HS) end_heads();
     }
     flush();
 }
@@ -2906,7 +3044,7 @@ struct Plan {
     size_t es;  // element size
     bool has_lb, exact, rev;
     bool f32f;  // TCDTW_FLAG_F32_FILTER: float64 inputs, float32 filter
-    size_t o_q32, o_c32, o_slack;
+    size_t o_q32, o_c32, o_slack, o_lanesc;
     int64_t max_tiles;
     // byte offsets
     size_t o_qT, o_ub, o_done, o_fin;
@@ -3033,6 +3171,8 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     const bool ti = dsc->method == TCDTW_METHOD_LB_TI ||
                     (dsc->method == TCDTW_METHOD_TC_DTW && dsc->advanced == TCDTW_METHOD_LB_TI);
     p.o_tisc = take(ti ? (size_t)p.adv_warps * 32 * 3 * p.B * es : 0);
+    p.o_lanesc = take(!p.exact && laner_rows_shape(p.n, p.d, p.B) > 0
+                          ? (size_t)kLanerMaxWarps * laner_scratch_words(p.B) * sizeof(float) : 0);
     p.o_q32 = take(p.f32f ? series_q : 0);
     p.o_c32 = take(p.f32f ? (size_t)N * p.n * p.d * 4 : 0);
     p.o_slack = take(p.f32f ? 32 : 0);
@@ -3144,6 +3284,7 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
     a.qpad_rows = p.qpad_rows;
     a.mg.add = nullptr;
     a.xq = a.xc = nullptr;
+    a.lane_scratch = (!p.exact && laner_rows_shape(p.n, p.d, p.B) > 0) ? at<float>(ws, p.o_lanesc) : nullptr;
     if (p.f32f) {  // queries / cands are the float32 copies in the workspace
         a.queries = at<T>(ws, p.o_q32);
         a.cands = at<T>(ws, p.o_c32);
