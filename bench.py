@@ -199,7 +199,7 @@ def index_envelope_stats(index, w, _lib, reps=5):
     peak = measured_peaks().get("hbm_gbs")
     gbs = nbytes / (t / 1e3) / 1e9
     del up, lo
-    return {"kernel": "envelope_stream_kernel", "bound": "hbm", "series": int(N), "ms": t,
+    return {"kernel": "envelope_vh_kernel (TMA bulk loads, van Herk in registers; k <= 32)", "bound": "hbm", "series": int(N), "ms": t,
             "algorithmic_bytes": nbytes, "achieved": gbs, "peak": peak, "unit": "GB/s",
             "frac": gbs / peak if peak else None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver copy test)"}

@@ -246,6 +246,192 @@ __global__ void __launch_bounds__(256) envelope_stream_kernel(const T* __restric
     asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// TMA-fed van Herk envelope (windows 2W+1 <= 32).  A persistent block walks
+// groups of G whole series.  One thread issues a TMA bulk copy
+// (cp.async.bulk, completion counted on an mbarrier) per series of the NEXT
+// group into the other of two shared-memory buffers while the current group
+// is processed; each series lands in a slot padded to 4 words mod 32, so
+// the lanes of a warp -- 8 series x 4 dimensions of one row -- hit distinct
+// banks.  Rows are indexed in v = row + W, cut into blocks of
+// k = 2W+1: the window of row i is v-block b = i / k from offset i % k plus
+// v-block b+1 up to offset i % k - 1 (van Herk / Gil-Werman).  One thread
+// per (series, dimension, block b): a backward scan of v-block b keeps its
+// suffix max/min in registers, a forward scan of v-block b+1 completes the k
+// outputs, staged in shared memory (same padded slots, conflict-free) and
+// streamed out with coalesced 16-byte stores.  Rows outside [0, n) are the identity, which clips
+// the window exactly as lb_mv.py:44-71.  Two block barriers per group of 8
+// series (staged outputs complete / stages free).
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+constexpr int kVhMaxK = 32;  // largest window (2W+1) of the register-resident van Herk path
+constexpr int kVhG = 8;      // series per group
+
+// Padded series slot, in elements: 4 words mod 32 (16-byte aligned TMA
+// destinations), so the 8 series of a group start in distinct bank quads.
+__host__ __device__ inline int vh_slot_elems(int nd, int es) {
+    int words = (nd * es / 4 + 3) & ~3;
+    words += (4 - words % 32 + 32) % 32;
+    return words * 4 / es;
+}
+
+template <typename T, int D, int KC>  // KC > 0: the window length 2W+1 as a compile-time constant
+__global__ void __launch_bounds__(512) envelope_vh_kernel(const T* __restrict__ S, int64_t n_series, int n, int w,
+                                                          T* __restrict__ U, T* __restrict__ Lo) {
+    extern __shared__ __align__(128) unsigned char vh_smem[];
+    const int nd = n * D;
+    const int SS = vh_slot_elems(nd, (int)sizeof(T));
+    T* buf = reinterpret_cast<T*>(vh_smem);                              // input [2][G][SS]
+    T* ou = buf + 2 * kVhG * SS;                                         // output stages [G][SS] (upper,
+    T* ol = ou + kVhG * SS;                                              // lower), same padded slots
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ol + kVhG * SS);        // 2 mbarriers
+    const int k = KC > 0 ? KC : 2 * w + 1;
+    constexpr int KU = KC > 0 ? KC : kVhMaxK;  // unrolled loop length
+    const int nb = (n + k - 1) / k;          // output blocks per series
+    const int tasks = kVhG * D * nb;         // (block, dim, series), series fastest
+    const unsigned ser_bytes = (unsigned)(nd * sizeof(T));
+    const T NEG = -dev_inf<T>(), POS = dev_inf<T>();
+    const int64_t stride = (int64_t)gridDim.x * kVhG;
+    auto issue = [&](int64_t s0, int slot) {  // one thread: TMA bulk copies of group s0
+        if (s0 >= n_series) return;
+        const int g = (int)((n_series - s0) < kVhG ? (n_series - s0) : kVhG);
+        mbar_expect(bar + slot, ser_bytes * g);
+        for (int j = 0; j < g; ++j)
+            tma_load_1d(buf + ((size_t)slot * kVhG + j) * SS, S + (s0 + j) * (int64_t)nd, ser_bytes, bar + slot);
+    };
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar + 1)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        issue((int64_t)blockIdx.x * kVhG, 0);
+        issue((int64_t)blockIdx.x * kVhG + stride, 1);
+    }
+    __syncthreads();
+    int it = 0;
+    for (int64_t s0 = (int64_t)blockIdx.x * kVhG; s0 < n_series; s0 += stride, ++it) {
+        const int slot = it & 1;
+        const int g_here = (int)((n_series - s0) < kVhG ? (n_series - s0) : kVhG);
+        mbar_wait(bar + slot, (unsigned)(it >> 1) & 1u);
+        const T* X = buf + (size_t)slot * kVhG * SS;
+        for (int t = threadIdx.x; t < tasks; t += blockDim.x) {
+            // series fastest: a warp's lanes read one row of 8 series x 4
+            // dimensions, one bank each (slots are 4 words mod 32 apart)
+            const int sr = t % kVhG;
+            const int p = (t / kVhG) % D;
+            const int b = t / (D * kVhG);
+            if (sr >= g_here) continue;
+            const T* x = X + (size_t)sr * SS + p;
+            // v-block b: rows r0 .. r0+k-1 with r0 = b*k - w; suffix extrema.
+            // Interior tasks (both v-blocks inside [0, n)) skip the range checks.
+            const int r0 = b * k - w;
+            const int r1 = r0 + k;  // first row of v-block b+1
+            const bool interior = r0 >= 0 && r1 + k - 1 < n;
+            T hx[KU], hn[KU];
+            T* du = ou + (size_t)sr * SS + p;
+            T* dl = ol + (size_t)sr * SS + p;
+            T gx = NEG, gn = POS;
+            if (interior) {
+                T mx = NEG, mn = POS;
+#pragma unroll
+                for (int j = KU - 1; j >= 0; --j) {
+                    if (KC > 0 || j < k) {
+                        const T v = x[(r0 + j) * D];
+                        mx = v > mx ? v : mx;
+                        mn = v < mn ? v : mn;
+                    }
+                    hx[j] = mx;
+                    hn[j] = mn;
+                }
+                // outputs i = b*k + j: h[j] (v-block b from offset j) with the
+                // prefix of v-block b+1 up to offset j-1 (all rows < n here)
+#pragma unroll
+                for (int j = 0; j < KU; ++j) {
+                    if (KC > 0 || j < k) {
+                        if (j > 0) {
+                            const T v = x[(r1 + j - 1) * D];
+                            gx = v > gx ? v : gx;
+                            gn = v < gn ? v : gn;
+                        }
+                        du[(b * k + j) * D] = gx > hx[j] ? gx : hx[j];
+                        dl[(b * k + j) * D] = gn < hn[j] ? gn : hn[j];
+                    }
+                }
+            } else {
+                T mx = NEG, mn = POS;
+#pragma unroll
+                for (int j = KU - 1; j >= 0; --j) {
+                    if (KC > 0 || j < k) {
+                        const int r = r0 + j;
+                        if ((unsigned)r < (unsigned)n) {
+                            const T v = x[r * D];
+                            mx = v > mx ? v : mx;
+                            mn = v < mn ? v : mn;
+                        }
+                    }
+                    hx[j] = mx;
+                    hn[j] = mn;
+                }
+#pragma unroll
+                for (int j = 0; j < KU; ++j) {
+                    if (KC > 0 || j < k) {
+                        const int i = b * k + j;
+                        if (j > 0) {
+                            const int r = r1 + j - 1;
+                            if ((unsigned)r < (unsigned)n) {
+                                const T v = x[r * D];
+                                gx = v > gx ? v : gx;
+                                gn = v < gn ? v : gn;
+                            }
+                        }
+                        if (i < n) {
+                            du[i * D] = gx > hx[j] ? gx : hx[j];
+                            dl[i * D] = gn < hn[j] ? gn : hn[j];
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();  // group consumed (its input buffer may be refilled), outputs staged
+        if (threadIdx.x == 0) issue(s0 + 2 * stride, slot);
+        // coalesced 16-byte streaming stores of the staged series
+        {
+            constexpr int VE = 16 / (int)sizeof(T);
+            using V4 = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+            const int nv = nd / VE;
+            for (int e = threadIdx.x; e < g_here * nv; e += blockDim.x) {
+                const int sr = e / nv, v = e - sr * nv;
+                const V4 xu = *reinterpret_cast<const V4*>(ou + (size_t)sr * SS + v * VE);
+                const V4 xl = *reinterpret_cast<const V4*>(ol + (size_t)sr * SS + v * VE);
+                __stcs(reinterpret_cast<V4*>(U + (s0 + sr) * (int64_t)nd) + v, xu);
+                __stcs(reinterpret_cast<V4*>(Lo + (s0 + sr) * (int64_t)nd) + v, xl);
+            }
+        }
+        __syncthreads();  // output stages free
+    }
+}
+
 // Sequential prefix sum with first-prefix abandoning (core.py:133-146).
 template <typename T>
 struct PrefixAbandon {
@@ -725,9 +911,61 @@ int pairs_lb_pc(int dtype, const void* c, const void* bl, const void* bh, int64_
     return dispatch_dtype_dims(dtype, d, LbPcPairsOp{}, c, bl, bh, P, n, d, G, K, gw, thr, out, ab, st);
 }
 
+// The TMA-fed van Herk path: windows up to 32 points, series whose bytes are
+// a 16-byte multiple, 16-byte aligned arrays.
+static int envelope_vh(int dtype, const void* s, int64_t ns, int n, int d, int w, void* u, void* l,
+                       cudaStream_t st) {
+    const int es = dtype == TCDTW_F64 ? 8 : 4;
+    if (2 * w + 1 > kVhMaxK || ((int64_t)n * d * es) % 16 != 0) return TCDTW_NOT_SUPPORTED;
+    if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(l)) & 15) != 0)
+        return TCDTW_NOT_SUPPORTED;
+    const size_t smem = (size_t)4 * kVhG * vh_slot_elems(n * d, es) * es + 16;
+    if (smem > 200 * 1024) return TCDTW_NOT_SUPPORTED;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // one thread per (series, dimension, block) task of a group
+    const int k = 2 * w + 1, tasks = kVhG * d * ((n + k - 1) / k);
+    int threads = (tasks + 31) / 32 * 32;
+    threads = threads > 512 ? 512 : threads;
+    auto go = [&](auto kern, auto* S, auto* U, auto* L) -> int {
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return TCDTW_NOT_SUPPORTED;
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        int64_t grid = (int64_t)(occ < 1 ? 1 : occ) * sms;
+        const int64_t groups = (ns + kVhG - 1) / kVhG;
+        if (grid > groups) grid = groups;
+        kern<<<(int)grid, threads, smem, st>>>(S, ns, n, w, U, L);
+        return launch_status();
+    };
+#define TCDTW_VH_K(DD, KK)                                                                              \
+    if (k == KK) {                                                                                      \
+        if (dtype == TCDTW_F64)                                                                         \
+            return go(envelope_vh_kernel<double, DD, KK>, (const double*)s, (double*)u, (double*)l);   \
+        return go(envelope_vh_kernel<float, DD, KK>, (const float*)s, (float*)u, (float*)l);           \
+    }
+#define TCDTW_VH(DD)                                                                                    \
+    if (d == DD) {                                                                                      \
+        TCDTW_VH_K(DD, 25) TCDTW_VH_K(DD, 13)                                                           \
+        if (dtype == TCDTW_F64)                                                                         \
+            return go(envelope_vh_kernel<double, DD, 0>, (const double*)s, (double*)u, (double*)l);    \
+        return go(envelope_vh_kernel<float, DD, 0>, (const float*)s, (float*)u, (float*)l);            \
+    }
+    TCDTW_VH(1) TCDTW_VH(2) TCDTW_VH(3) TCDTW_VH(4) TCDTW_VH(5) TCDTW_VH(6) TCDTW_VH(8) TCDTW_VH(20)
+#undef TCDTW_VH
+#undef TCDTW_VH_K
+    return TCDTW_NOT_SUPPORTED;
+}
+
 int series_envelope(int dtype, const void* s, int64_t ns, int n, int d, int w, void* u, void* l,
                     cudaStream_t st) {
     if (ns <= 0) return TCDTW_OK;
+    {
+        const int r = envelope_vh(dtype, s, ns, n, d, w, u, l, st);
+        if (r != TCDTW_NOT_SUPPORTED) return r;
+    }
     const int64_t total = ns * (int64_t)n * d;
     const size_t es = dtype == TCDTW_F64 ? 8 : 4;
     const size_t per_series = (size_t)6 * n * d * es;  // 2 staging + 4 scan arrays

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_index.py tests/test_gpu_reference_properties.py -m gpu -x -q > gpurun_out/r2e_tests.log 2>&1; echo "exit=$?" >> gpurun_out/r2e_tests.log
+timeout 300 python bench.py --queries 1000 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r2e_c4_1k.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"envelope_vh" -s 1 -c 1 -o gpurun_out/r2e_env python bench.py --queries 256 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/r2e_ncu.log 2>&1
+echo "ncu exit=$?" >> gpurun_out/r2e_ncu.log
