@@ -177,6 +177,12 @@ typedef struct tcdtw_search_desc {
  * with TCDTW_FLAG_REVERSE_LB. */
 #define TCDTW_FLAG_F32_FILTER 4
 #define TCDTW_FLAG_DEBUG_SYNC 8 /* synchronise + report to stderr after every stage */
+/* Prune / abandon against a snapshot of d_best taken before each DTW pass
+ * instead of the live value other DTWs keep tightening: the same answers,
+ * somewhat more DP cells, and dtw_cells / abandon_count identical from run
+ * to run -- what the reference's deterministic work model (search.py:14-19,
+ * 102-125) needs when tuning or selecting on the GPU's counters. */
+#define TCDTW_FLAG_FROZEN_THRESHOLDS 16
 #define TCDTW_PHASES 8      /* prep, lb_mv, seeds_topk, seeds_dtw, compact, advanced, dtw, finalize */
 #define TCDTW_COUNTERS 9    /* per query: see enum below */
 

@@ -26,6 +26,7 @@ FLAG_TIMING = 1
 FLAG_REVERSE_LB = 2
 FLAG_F32_FILTER = 4
 FLAG_DEBUG_SYNC = 8
+FLAG_FROZEN_THRESHOLDS = 16
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64

@@ -685,6 +685,10 @@ struct SArgs {
     const T* env_up;      // (Q, n, d) query envelopes (nullptr without LB_MV)
     const T* env_lo;
     T* dbest;             // (Q,)
+    // where the prune / abandon thresholds are read: dbest (live: every
+    // completed DTW tightens them), or a snapshot taken before each DTW pass
+    // (TCDTW_FLAG_FROZEN_THRESHOLDS: run-to-run identical cell counts)
+    const T* thr_src;
     const T* box_lo;      // (Q, G, K, d)
     const T* box_hi;
     const T* qsteps;      // (Q, n-1)
@@ -779,7 +783,7 @@ __global__ void __launch_bounds__(256) dtw_tpp_kernel(SArgs<T> a, Tiles tl, int6
         T band[BMAX];
 #pragma unroll
         for (int k = 0; k < BMAX; ++k) band[k] = (k == w) ? T(0) : INF;
-        T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg) : INF;
+        T thr = a.abandon ? scale_up<T>(load_volatile(a.thr_src + q), a.mg) : INF;
         bool done = !active;
         int stop_row = n - 1;
         bool abandoned = false;
@@ -854,7 +858,7 @@ __global__ void __launch_bounds__(256) dtw_tpp_kernel(SArgs<T> a, Tiles tl, int6
                 stop_row = i;
             }
             if (__all_sync(0xffffffffu, done)) break;
-            if ((i & 7) == 7 && a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg);
+            if ((i & 7) == 7 && a.abandon) thr = scale_up<T>(load_volatile(a.thr_src + q), a.mg);
 #pragma unroll
             for (int p = 0; p < DMAX; ++p) cpt[p] = cnext[p];
         }
@@ -1188,7 +1192,7 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
                     pf_lb = casc ? a.lb[(int64_t)t_q * a.N + pf_c] : T(0);
                     load_pair(pf_pair, a.cands + (int64_t)pf_c * n * D, 0);
                 }
-                t_thr_raw = a.abandon ? load_volatile(a.dbest + t_q) : INF;
+                t_thr_raw = a.abandon ? load_volatile(a.thr_src + t_q) : INF;
                 if (t_q != staged_q) {
                     __syncwarp();
                     const T* qs = a.queries + (int64_t)t_q * n * D;
@@ -1356,7 +1360,7 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
             // the best-so-far read issued 8 rows ago; issue the next one
             since = 0;
             thr = scale_up<T>(thr_pend_raw, a.mg);
-            if (a.abandon) thr_pend_raw = load_volatile(a.dbest + q);
+            if (a.abandon) thr_pend_raw = load_volatile(a.thr_src + q);
         }
     };
     // One copy of the step keeps the body inside the 32 KB L1.5 I-cache;
@@ -1563,7 +1567,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
             pf_res = res[e];
             pf_lb = casc ? a.lb[(int64_t)t_q * a.N + pf_c] : 0.f;
         }
-        t_thr_raw = a.abandon ? load_volatile(a.dbest + t_q) : INF;
+        t_thr_raw = a.abandon ? load_volatile(a.thr_src + t_q) : INF;
     };
     auto load_query = [&](int q) {  // the warp's query slot (all lanes idle)
         __syncwarp();
@@ -1641,7 +1645,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                     load_rows(c, cand, i);
 #pragma unroll
                     for (int k = 0; k < B; ++k) ps[k * 32] = queue_band[k * 32 + sl];
-                    const float raw = a.abandon ? load_volatile(a.dbest + slot_q) : INF;
+                    const float raw = a.abandon ? load_volatile(a.thr_src + slot_q) : INF;
                     thr = a.abandon ? scale_up<float>(raw, a.mg) : INF;
                     thr_pend_raw = raw;
                     since = 0;
@@ -1728,7 +1732,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
             prefix = park_pre[lane];
 #pragma unroll
             for (int k = 0; k < B; ++k) ps[k * 32] = park_band[k * 32];
-            const float raw = a.abandon ? load_volatile(a.dbest + slot_q) : INF;
+            const float raw = a.abandon ? load_volatile(a.thr_src + slot_q) : INF;
             thr = a.abandon ? scale_up<float>(raw, a.mg) : INF;
             thr_pend_raw = raw;
 #pragma unroll
@@ -1872,7 +1876,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                 if (since >= a.thr_every) {
                     since = 0;
                     thr = scale_up<float>(thr_pend_raw, a.mg);
-                    if (a.abandon) thr_pend_raw = load_volatile(a.dbest + cq);
+                    if (a.abandon) thr_pend_raw = load_volatile(a.thr_src + cq);
                 }
             }
         }
@@ -1985,7 +1989,7 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
             const T* crow = a.cands + c * (int64_t)n * d;
             for (int k = lane; k < B; k += 32) prow[k] = (k == w) ? T(0) : INF;
             __syncwarp();
-            T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg) : INF;
+            T thr = a.abandon ? scale_up<T>(load_volatile(a.thr_src + q), a.mg) : INF;
             T fin = INF;
             bool abandoned = false;
             int stop_row = n - 1;
@@ -2042,7 +2046,7 @@ __global__ void __launch_bounds__(256) dtw_wave_kernel(SArgs<T> a, Tiles tl, int
                     stop_row = i0 + first;
                     break;
                 }
-                if (a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg);
+                if (a.abandon) thr = scale_up<T>(load_volatile(a.thr_src + q), a.mg);
             }
             fin = __shfl_sync(0xffffffffu, fin, (n - 1) & 31);
             if (!abandoned && fin > thr) abandoned = true;  // dtw.py:101-102
@@ -2155,7 +2159,7 @@ __global__ void __launch_bounds__(256, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
             const T* crow = a.cands + c * (int64_t)n * D;
             for (int k = lane; k < PR; k += 32) prow[k] = (k == w) ? T(0) : INF;
             __syncwarp();
-            T thr = a.abandon ? scale_up<T>(load_volatile(a.dbest + q), a.mg) : INF;
+            T thr = a.abandon ? scale_up<T>(load_volatile(a.thr_src + q), a.mg) : INF;
             bool abandoned = false;
             int stop_row = n - 1;
             for (int i0 = 0; i0 < n; i0 += 32) {
@@ -2234,7 +2238,7 @@ __global__ void __launch_bounds__(256, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
                     stop_row = i0 + __ffs(bad) - 1;
                     break;
                 }
-                if (a.abandon) thr = scale_up<T>(load_volatile(a.dbest + q), a.mg);
+                if (a.abandon) thr = scale_up<T>(load_volatile(a.thr_src + q), a.mg);
             }
             const T fin = abandoned ? INF : prow[w];  // row n-1, column n-1
             if (!abandoned && fin > thr) abandoned = true;  // dtw.py:101-102
@@ -2286,7 +2290,7 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
         const int64_t ent = tl.begin[tile] + lane;
         const bool has = lane < tl.len[tile];
         const int64_t c = has ? (int64_t)cand_of[ent] : 0;
-        const T db = load_volatile(a.dbest + q);
+        const T db = load_volatile(a.thr_src + q);
         const T thr = scale_up<T>(db, a.mg);
         const T lb1 = has ? a.lb[q * a.N + c] : T(0);
         // trigger band: b1 > e * d_best (search.py:147); EXACT uses the
@@ -2485,7 +2489,7 @@ __global__ void __launch_bounds__(256) advanced_pc_kernel(SArgs<T> a, Tiles tl, 
             __syncwarp();
         }
         const int64_t c = has ? (int64_t)cand_of[ent] : 0;
-        const T db = load_volatile(a.dbest + q);
+        const T db = load_volatile(a.thr_src + q);
         const T thr = scale_up<T>(db, a.mg);
         const T lb1 = has ? a.lb[q * a.N + c] : T(0);
         const bool go = has && !(res[ent] < T(0)) && (lb1 > a.trigger * db);  // trigger band, search.py:147
@@ -3044,7 +3048,7 @@ struct Plan {
     size_t es;  // element size
     bool has_lb, exact, rev;
     bool f32f;  // TCDTW_FLAG_F32_FILTER: float64 inputs, float32 filter
-    size_t o_q32, o_c32, o_slack, o_lanesc;
+    size_t o_q32, o_c32, o_slack, o_lanesc, o_dbf;
     int64_t max_tiles;
     // byte offsets
     size_t o_qT, o_ub, o_done, o_fin;
@@ -3127,6 +3131,7 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     p.o_seedres = take((size_t)Q * kSeedMax * es);
     p.o_seedcnt = take((size_t)Q * 4);
     p.o_dbest = take((size_t)Q * es);
+    p.o_dbf = take((size_t)Q * es);
     p.o_ccnt = take((size_t)Q * p.n_chunks * 8);
     p.o_coff = take(((size_t)Q * p.n_chunks + 1) * 8);
     p.o_surv = take((size_t)Q * N * 4);
@@ -3239,6 +3244,7 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
     a.env_up = p.has_lb ? at<T>(ws, p.o_up) : nullptr;
     a.env_lo = p.has_lb ? at<T>(ws, p.o_lo) : nullptr;
     a.dbest = at<T>(ws, p.o_dbest);
+    a.thr_src = (dsc->flags & TCDTW_FLAG_FROZEN_THRESHOLDS) ? at<T>(ws, p.o_dbf) : a.dbest;
     a.box_lo = at<T>(ws, p.o_blo);
     a.box_hi = at<T>(ws, p.o_bhi);
     a.qsteps = at<T>(ws, p.o_steps);
@@ -3512,6 +3518,8 @@ struct SearchImpl {
             TRY(launch_status());
             dbg_stage(dsc, st, "topk+tiles");
             tm.mark(3);
+            if (a.thr_src != a.dbest)  // frozen thresholds: the seed pass prunes against the UB seeding
+                cudaMemcpyAsync(const_cast<T*>(a.thr_src), a.dbest, (size_t)p.Q * sizeof(T), cudaMemcpyDeviceToDevice, st);
             TRY((launch_dtw<T, DMAX, EXACT>(a, p, stl, p.Q, seeds, at<T>(ws, p.o_seedres), at<int>(ws, p.o_tctr), st,
                                             few_pairs(p.Q * (int64_t)p.S))));
         } else {
@@ -3539,6 +3547,8 @@ struct SearchImpl {
         tm.mark(4);
         if (dbest_in && dbest_in != (const void*)a.dbest)
             cudaMemcpyAsync(a.dbest, dbest_in, (size_t)p.Q * sizeof(T), cudaMemcpyDeviceToDevice, st);
+        if (a.thr_src != a.dbest)  // frozen thresholds: the best after the seed phase (and the exchange)
+            cudaMemcpyAsync(const_cast<T*>(a.thr_src), a.dbest, (size_t)p.Q * sizeof(T), cudaMemcpyDeviceToDevice, st);
         // compaction
         const bool all = !p.has_lb;
         int64_t* ccnt = at<int64_t>(ws, p.o_ccnt);

@@ -161,6 +161,8 @@ class SearchIndex:
             self.f32_filter = False
         self.base = int(base)
         self.done_cap = 0  # completed-DTW list capacity (0 = library default; tests force 1)
+        # thresholds frozen per DTW pass: run-to-run identical cell counts (work-model tuning)
+        self.frozen_thresholds = False
         self._ws = None
         self._ws_bytes = 0
         self._cenv = None  # (window, upper, lower): candidate-side index
@@ -202,6 +204,8 @@ class SearchIndex:
               phase_buf, reverse_bound: bool = False) -> _lib.SearchDesc:
         _, n, d = self.candidates.shape
         flags = _lib.FLAG_TIMING if timing else 0
+        if self.frozen_thresholds:
+            flags |= _lib.FLAG_FROZEN_THRESHOLDS
         rev = reverse_bound and params.method != Method.NONE
         if self._filtering(rev):
             flags |= _lib.FLAG_F32_FILTER
@@ -415,8 +419,12 @@ def _run_sample(queries, candidates, params, advanced, dim_range, metric) -> flo
         return 0.0
     adv = _advanced_method(params, advanced)
     qarr = np.stack([as_series(q) for q in queries])
-    res = SearchIndex(np.asarray(_stack(candidates), dtype=np.float64), dtype="f64").search(
-        qarr, params, advanced=advanced, dim_range=dim_range, timing=(metric == "time"))
+    index = SearchIndex(np.asarray(_stack(candidates), dtype=np.float64), dtype="f64")
+    # the work model reads DP-cell counts: freeze the thresholds per DTW pass
+    # so that one seed gives the same choice and counters on every run (the
+    # reference's guarantee, search.py:14-19)
+    index.frozen_thresholds = metric != "time"
+    res = index.search(qarr, params, advanced=advanced, dim_range=dim_range, timing=(metric == "time"))
     n, dims = qarr.shape[1:]
     if metric == "time":
         return float(sum(res.phase_ms.values())) / 1e3

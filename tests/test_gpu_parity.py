@@ -402,6 +402,37 @@ def test_tc_dtw_select_and_tune(P):
         assert (out.best_index, out.best_distance) == (ref.best_index, ref.best_distance)
 
 
+def test_work_model_is_run_to_run_deterministic(P):
+    """with metric="work" the choices and the DP-cell counters must
+    not depend on the timing of other DTWs' best-so-far updates.  A sample
+    of 8 queries x 40 candidates (more than the 23 the tuner draws), three
+    repetitions: identical tune_params / tc_dtw_select results, identical
+    work-model costs, identical dtw_cells and abandon_count."""
+    from paper_2101_07731_b200.search import SearchIndex
+
+    rng = np.random.default_rng(17)
+    series = np.cumsum(rng.normal(size=(48, 96, 3)), axis=1)
+    queries, cands = list(series[:8]), list(series[8:])
+    params = P.SearchParams(window=9, method="tc_dtw")
+    runs = []
+    for _ in range(3):
+        log = []
+        tuned = P.tune_params(queries, cands, params, seed=2, log=log)
+        choice = P.tc_dtw_select(queries, cands, tuned)
+        runs.append((tuned, choice, [c for _, _, c in log]))
+    assert all(r == runs[0] for r in runs[1:])
+    ctrs = []
+    for _ in range(3):
+        idx = SearchIndex(np.stack(cands), dtype="f64")
+        idx.frozen_thresholds = True
+        res = idx.search(np.stack(queries), P.SearchParams(window=9, method="lb_mv"))
+        ctrs.append((res.counters["dtw_cells"].tolist(), res.counters["abandon_count"].tolist(),
+                     res.best_index.tolist(), res.best_distance.tolist()))
+    assert all(c == ctrs[0] for c in ctrs[1:])
+    live = SearchIndex(np.stack(cands), dtype="f64").search(np.stack(queries), P.SearchParams(window=9, method="lb_mv"))
+    assert live.best_index.tolist() == ctrs[0][2] and live.best_distance.tolist() == ctrs[0][3]
+
+
 def test_gpu_cost_selection(P):
     """Row f1: selection and tuning ranked by measured GPU phase times
     (metric="time") instead of the work model; answers never change."""
