@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exchange", action="store_true", help="skip the d_best all-reduce between phases")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (testing)")
+    ap.add_argument("--no-cascade", action="store_true", help="A/B: DTW abandons on row minima only")
     ap.add_argument("--reverse-bound", action="store_true",
                     help="also prune on LB_MV(q, env(c)) from the candidate-side index (SURVEY 8f f2)")
     return ap.parse_args()
@@ -340,6 +341,7 @@ def run_ours(args):
     params, advanced = resolve_method(P, wl, w, args.method, wl.dim_range)
     t_up = time.perf_counter()
     index = P.SearchIndex(wl.candidates[a:b], dtype=wl.dtype, base=a)
+    index.cascade = not args.no_cascade
     torch.cuda.synchronize()
     t_up = time.perf_counter() - t_up
     env_stats = index_envelope_stats(index, w, _lib)
@@ -478,7 +480,7 @@ def run_ours(args):
                        "advanced": None if advanced is None else advanced.value,
                        "trigger_ti": params.trigger_ti, "trigger_pc": params.trigger_pc,
                        "quant_levels": params.quant_levels, "query_batch": batch,
-                       "reverse_bound": bool(args.reverse_bound),
+                       "reverse_bound": bool(args.reverse_bound), "cascade": not args.no_cascade,
                        "parallelism": f"candidate shards x{world}",
                        "l2": "inputs larger than L2 (collection resident in HBM, no flush)"},
             "e2e": {"value": n_q / (e2e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": q_bytes,

@@ -163,6 +163,11 @@ typedef struct tcdtw_search_desc {
      * default); when it overflows, every survivor tile is scanned instead.
      * Tests set 1 to exercise that path (ABI version 3). */
     int64_t done_cap;
+    /* Optional (ABI version 3): the candidates in the planar layout the
+     * LB_MV pass reads, (n * dims, n_candidates) of `dtype`, made once per
+     * collection with tcdtw_planarize; NULL = planarised into the workspace
+     * on every call.  Ignored with TCDTW_FLAG_F32_FILTER. */
+    const void *cand_planar;
 } tcdtw_search_desc;
 
 #define TCDTW_FLAG_TIMING 1     /* fill desc->phase_ms (synchronises the stream) */
@@ -183,6 +188,9 @@ typedef struct tcdtw_search_desc {
  * to run -- what the reference's deterministic work model (search.py:14-19,
  * 102-125) needs when tuning or selecting on the GPU's counters. */
 #define TCDTW_FLAG_FROZEN_THRESHOLDS 16
+/* DTW abandons on its row minima only, without the LB_MV suffix cascade
+ * (an A/B knob: the same answers, more DP cells). */
+#define TCDTW_FLAG_NO_CASCADE 32
 #define TCDTW_PHASES 8      /* prep, lb_mv, seeds_topk, seeds_dtw, compact, advanced, dtw, finalize */
 #define TCDTW_COUNTERS 9    /* per query: see enum below */
 
@@ -226,6 +234,11 @@ int tcdtw_search_finish(const tcdtw_search_desc *desc, const void *queries, cons
 int tcdtw_nn_search(const tcdtw_search_desc *desc, const void *queries, const void *candidates,
                     const void *dim_range, void *workspace, size_t ws_bytes, int64_t *best_index,
                     double *best_distance, int64_t *counters, void *stream);
+
+/* The planar copy of a collection for tcdtw_search_desc.cand_planar:
+ * series (n_series, n, dims) -> out (n * dims, n_series), dtype elements. */
+int tcdtw_planarize(int dtype, const void *series, int64_t n_series, int32_t n, int32_t dims, void *out,
+                    void *stream);
 
 /* Cross-shard combine (no reference counterpart -- the
  * reference is single-process).  records (world, n_queries, 2)

@@ -27,6 +27,7 @@ FLAG_REVERSE_LB = 2
 FLAG_F32_FILTER = 4
 FLAG_DEBUG_SYNC = 8
 FLAG_FROZEN_THRESHOLDS = 16
+FLAG_NO_CASCADE = 32
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -47,7 +48,7 @@ class SearchDesc(ctypes.Structure):
         ("min_cell_frac", ctypes.c_double), ("n_queries", _i64), ("n_candidates", _i64),
         ("candidate_base", _i64), ("seeds", _i32), ("flags", _i32),
         ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("cand_upper", _vp), ("cand_lower", _vp),
-        ("done_cap", _i64),
+        ("done_cap", _i64), ("cand_planar", _vp),
     ]
 
 
@@ -83,6 +84,7 @@ _SIGS = {
                              _vp], ctypes.c_int),
     "tcdtw_nn_search": ([ctypes.POINTER(SearchDesc), _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp],
                         ctypes.c_int),
+    "tcdtw_planarize": ([ctypes.c_int, _vp, _i64, _i32, _i32, _vp, _vp], ctypes.c_int),
     "tcdtw_shard_combine": ([_vp, _i32, _i64, _vp, _vp, _vp], ctypes.c_int),
     "tcdtw_lb_mv_matrix": ([ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp], ctypes.c_int),
     "tcdtw_dtw_kernel_name": ([ctypes.POINTER(SearchDesc)], ctypes.c_char_p),

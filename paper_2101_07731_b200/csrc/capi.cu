@@ -37,6 +37,7 @@ const char* dtw_kernel_name(const tcdtw_search_desc*);
 size_t normalize_workspace_bytes(int64_t, int);
 int normalize_f64(const double*, int64_t, int, double*, double*, double*, double*, double*, cudaStream_t);
 int shard_combine(const int64_t*, int, int64_t, int64_t*, double*, cudaStream_t);
+int planarize_series(int, const void*, int64_t, int, int, void*, cudaStream_t);
 }  // namespace tcdtw
 
 using namespace tcdtw;
@@ -207,6 +208,14 @@ int tcdtw_normalize(const double* values, int64_t n_points, int32_t dims, double
     if (!workspace || ws_bytes < normalize_workspace_bytes(n_points, dims)) return TCDTW_WORKSPACE_TOO_SMALL;
     return normalize_f64(values, n_points, dims, out, mean, std_, range, (double*)workspace, S(stream));
 }
+int tcdtw_planarize(int dtype, const void* series, int64_t n_series, int32_t n, int32_t dims, void* out,
+                    void* stream) {
+    if (!dtype_ok(dtype) || n_series < 0 || n < 1 || dims < 1) return TCDTW_INVALID_INPUT;
+    if (n_series > 0 && (!series || !out)) return TCDTW_INVALID_INPUT;
+    if (n_series == 0) return TCDTW_OK;
+    return planarize_series(dtype, series, n_series, n, dims, out, S(stream));
+}
+
 int tcdtw_shard_combine(const int64_t* records, int32_t world, int64_t n_queries, int64_t* best_index,
                         double* best_distance, void* stream) {
     if (world < 1 || n_queries < 0 || (n_queries > 0 && (!records || !best_index || !best_distance)))

@@ -79,6 +79,12 @@ const char* dtw_kernel_name(const tcdtw_search_desc* dsc) {
     return "dtw_wave_kernel";
 }
 
+int planarize_series(int dtype, const void* series, int64_t ns, int n, int d, void* out, cudaStream_t st) {
+    if (dtype == TCDTW_F64) return planarize<double>((const double*)series, ns, n * d, (double*)out, st);
+    if (dtype == TCDTW_F32) return planarize<float>((const float*)series, ns, n * d, (float*)out, st);
+    return TCDTW_INVALID_INPUT;
+}
+
 int alu_probe(int dtype, int blocks, int iters, void* sink, double* lane_ops, cudaStream_t st) {
     if (dtype == TCDTW_F64) alu_probe_kernel<double><<<blocks, 256, 0, st>>>(iters, (double*)sink);
     else alu_probe_kernel<float><<<blocks, 256, 0, st>>>(iters, (float*)sink);

@@ -153,7 +153,7 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
                                                         const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                         int64_t Q, int64_t N, int n, int d, int TC,
                                                         T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
-                                                        int64_t c0, bool v16, bool trans);
+                                                        int64_t c0, bool v16, bool trans, int64_t ub_n, int ub_stride);
 
 // asynchronous global -> shared copies; src_bytes < bytes zero-fills the rest
 __device__ __forceinline__ void cp_async_ca(void* dst, const void* src, int bytes, int src_bytes) {
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ 
                                                           const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                           int64_t Q, int64_t N, int n, int d, int TC,
                                                           T* __restrict__ out, T* __restrict__ ub_out, int ub_stride,
-                                                          bool v16, bool trans) {
+                                                          bool v16, bool trans, int64_t ub_n) {
     using Tile = MvTile<T, DMAX, EXACT>;
     constexpr int QT = Tile::QT, CTL = Tile::CT;
     // query tiles vary fastest: concurrently resident blocks share one
@@ -192,12 +192,12 @@ __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ 
     if constexpr (UB) {
         if (((int64_t)blockIdx.x / nqt) % ub_stride != 0) {
             lbmv_matrix_kernel_body<T, DMAX, EXACT, false, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0,
-                                                               v16, trans);
+                                                               v16, trans, ub_n, ub_stride);
             return;
         }
     }
     lbmv_matrix_kernel_body<T, DMAX, EXACT, UB, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0, v16,
-                                                    trans);
+                                                    trans, ub_n, ub_stride);
 }
 
 template <typename T, int DMAX, bool EXACT, bool UB, int DX>
@@ -205,7 +205,7 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
                                                         const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                         int64_t Q, int64_t N, int n, int d, int TC,
                                                         T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
-                                                        int64_t c0, bool v16, bool trans) {
+                                                        int64_t c0, bool v16, bool trans, int64_t ub_n, int ub_stride) {
     using Tile = MvTile<T, DMAX, EXACT>;
     constexpr int M = Tile::M, QT = Tile::QT, CTL = Tile::CT;
     constexpr int VN = 16 / (int)sizeof(T);  // elements per 16-byte copy
@@ -388,7 +388,9 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
                 // trans: the reverse bound (envelope side = candidates) lands
                 // in the (query, candidate) layout of the forward matrix
                 out[trans ? c * Q + q : q * N + c] = total[i][j];
-                if constexpr (UB) ub_out[q * N + c] = ubt[i][j];
+                // upper bounds only on the sampled candidate tiles, stored
+                // compactly: (q, sampled tile, column) -> q * ub_n + ...
+                if constexpr (UB) ub_out[q * ub_n + (c0 / CTL / ub_stride) * CTL + (c - c0)] = ubt[i][j];
             }
         }
     }
@@ -396,7 +398,7 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
 
 template <typename T, int DMAX, bool EXACT>
 int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int64_t Q, int64_t N, int n, int d,
-                       T* out, T* ub_out, cudaStream_t st, int ub_stride = 1, bool trans = false) {
+                       T* out, T* ub_out, cudaStream_t st, int ub_stride = 1, bool trans = false, int64_t ub_n = 0) {
     using Tile = MvTile<T, DMAX, EXACT>;
     const bool ub = ub_out != nullptr;
     // two staging buffers of TC time steps each (layout us | ls | cs | qs)
@@ -426,7 +428,7 @@ int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int6
     const int64_t nct = (N + Tile::CT - 1) / Tile::CT;
     if (nqt * nct > 2147483647LL) return TCDTW_NOT_SUPPORTED;
     const unsigned grid = (unsigned)(nqt * nct);
-    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out, ub_stride, v16, trans);
+    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out, ub_stride, v16, trans, ub_n);
     return launch_status();
 }
 
@@ -436,7 +438,9 @@ __global__ void __launch_bounds__(256) topk_kernel(const T* __restrict__ lb, int
                                                    uint32_t* __restrict__ seeds, int32_t* __restrict__ seed_cnt,
                                                    int ct, int stride) {
     const int64_t q = blockIdx.x;
-    const T* row = lb + q * N;
+    const int64_t ub_n = ((N / ((int64_t)ct * stride)) * ct) +
+                         ((N % ((int64_t)ct * stride)) < ct ? (N % ((int64_t)ct * stride)) : ct);  // sampled columns
+    const T* row = lb + q * ub_n;
     T bv[S];
     uint32_t bi[S];
 #pragma unroll
@@ -444,11 +448,10 @@ __global__ void __launch_bounds__(256) topk_kernel(const T* __restrict__ lb, int
         bv[k] = dev_inf<T>();
         bi[k] = 0xffffffffu;
     }
-    // keys exist on every stride-th tile of ct candidates
-    for (int64_t k = threadIdx.x;; k += blockDim.x) {
+    // keys exist on every stride-th tile of ct candidates, stored compactly
+    for (int64_t k = threadIdx.x; k < ub_n; k += blockDim.x) {
         const int64_t c = (k / ct) * ct * stride + (k % ct);
-        if (c >= N) break;
-        const T v = row[c];
+        const T v = row[k];
         if (v < bv[S - 1]) {
             bv[S - 1] = v;
             bi[S - 1] = (uint32_t)c;
@@ -700,6 +703,7 @@ struct SArgs {
     Margins mg;
     bool abandon;         // false for Method.NONE (search.py:135)
     T casc_lo, casc_hi, casc_thr;  // cascaded-abandon slack (see dtw_tpp_kernel)
+    bool cascade;         // abandon on the LB_MV suffix too (off: TCDTW_FLAG_NO_CASCADE)
     // completed (not abandoned) DTWs, (q << 40 | entry), so the finalisation
     // visits only them; nullptr for the seed pass
     unsigned long long* done_list;
@@ -793,7 +797,7 @@ __global__ void __launch_bounds__(256) dtw_tpp_kernel(SArgs<T> a, Tiles tl, int6
         // cost >= that row's LB_MV term, so DTW >= rowmin_i + sum_{r>i} term_r
         // (the LB_MV row sum is LB[q][c]).  The suffix is estimated from below
         // with the relative slack a.casc (rounding of both sums).
-        const bool casc = a.lb != nullptr && a.abandon;
+        const bool casc = a.lb != nullptr && a.abandon && a.cascade;
         const T lbtot = (casc && active) ? a.lb[q * a.N + c] : T(0);
         const T* eu = casc ? a.env_up + q * (int64_t)n * d : nullptr;
         const T* el = casc ? a.env_lo + q * (int64_t)n * d : nullptr;
@@ -1062,7 +1066,7 @@ __global__ void __launch_bounds__(64) dtw_lane_kernel(SArgs<T> a, Tiles tl, int6
     int staged_q = -1;
     const unsigned FULL = 0xffffffffu;
     const T INF = dev_inf<T>();
-    const bool casc = a.lb != nullptr && a.abandon;
+    const bool casc = a.lb != nullptr && a.abandon && a.cascade;
     // warp reservoir (uniform) with per-tile prefetch held one entry per lane
     int64_t t_begin = 0;
     int t_q = -1, t_len = 0, t_next = 0;
@@ -1502,7 +1506,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     float* const ps = es + L::e_words(n) + lane;                           // band row: slot k at ps[k*32]
     const unsigned FULL = 0xffffffffu;
     const float INF = dev_inf<float>();
-    const bool casc = CASC && a.lb != nullptr && a.abandon && a.env_up != nullptr;
+    const bool casc = CASC && a.lb != nullptr && a.abandon && a.env_up != nullptr && a.cascade;
     const bool heads = HS > 0 && n > R * (HS + 1) && a.lane_scratch != nullptr;
     float* const scr = a.lane_scratch + (size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * laner_scratch_words(B);
     float* const park_band = scr + lane;
@@ -3048,6 +3052,7 @@ struct Plan {
     size_t es;  // element size
     bool has_lb, exact, rev;
     bool f32f;  // TCDTW_FLAG_F32_FILTER: float64 inputs, float32 filter
+    bool cand_planar;  // desc->cand_planar is used instead of o_candT
     size_t o_q32, o_c32, o_slack, o_lanesc, o_dbf;
     int64_t max_tiles;
     // byte offsets
@@ -3116,14 +3121,15 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     p.o_upT = take(p.has_lb ? series_q : 0);
     p.o_loT = take(p.has_lb ? series_q : 0);
     p.o_qT = take(p.has_lb ? series_q : 0);
-    p.o_candT = take(p.has_lb ? (size_t)N * p.n * p.d * es : 0);
+    p.cand_planar = p.has_lb && dsc->cand_planar != nullptr && !p.f32f;  // the caller keeps a planar copy
+    p.o_candT = take(p.has_lb && !p.cand_planar ? (size_t)N * p.n * p.d * es : 0);
     p.o_steps = take((size_t)Q * (p.n > 1 ? p.n - 1 : 1) * es);
     const size_t boxes = (size_t)Q * p.G * p.K * p.d * es;
     p.o_blo = take(boxes);
     p.o_bhi = take(boxes);
     p.o_bcnt = take((size_t)Q * p.G * 4);
     p.o_lb = take(p.has_lb ? (size_t)Q * N * es : 0);
-    p.o_ub = take(p.has_lb ? (size_t)Q * N * es : 0);
+    p.o_ub = 0;  // sized below, once the sampling is known
     p.o_cupT = take(p.rev ? (size_t)N * p.n * p.d * es : 0);
     p.o_cloT = take(p.rev ? (size_t)N * p.n * p.d * es : 0);
     p.o_lb2 = take(p.rev ? (size_t)Q * N * es : 0);
@@ -3161,6 +3167,7 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
         const int64_t rem = N % ((int64_t)p.ub_ct * p.ub_stride);
         p.ub_sampled = full + (rem < p.ub_ct ? rem : p.ub_ct);
     }
+    p.o_ub = take(p.has_lb ? (size_t)Q * p.ub_sampled * es : 0);  // the sampled upper bounds, compact
     if (dsc->done_cap > 0) p.done_cap = dsc->done_cap;  // tests force the overflow path with 1
     p.o_done = take((size_t)p.done_cap * 8 + 64);
     p.fin_cap = p.done_cap + Q * kSeedMax;
@@ -3281,6 +3288,7 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
         a.casc_thr = (T)1.0;  // thr already carries the (1+3 eps) margin
     }
     a.abandon = dsc->method != TCDTW_METHOD_NONE;
+    a.cascade = (dsc->flags & TCDTW_FLAG_NO_CASCADE) == 0;
     a.refill_min = 8;
     a.thr_every = 8;  // re-reading the live d_best every 4 / 8 / 16 rows measured equal (C4)
     a.done_list = nullptr;  // set for the survivors pass only
@@ -3461,12 +3469,13 @@ struct SearchImpl {
         cudaMemsetAsync(at<char>(ws, p.o_ctr), 0, (size_t)p.Q * TCDTW_COUNTERS * 8, st);
         fill_kernel<T><<<grid_for(p.Q, 256), 256, 0, st>>>(a.dbest, p.Q, dev_inf<T>());
         TRY(launch_status());
+        const T* candT = p.cand_planar ? (const T*)dsc->cand_planar : at<T>(ws, p.o_candT);
         if (p.has_lb) {
             TRY(series_envelope(dtype, queries, p.Q, p.n, p.d, p.w, at<T>(ws, p.o_up), at<T>(ws, p.o_lo), st));
             TRY(planarize<T>(at<T>(ws, p.o_up), p.Q, p.n * p.d, at<T>(ws, p.o_upT), st));
             TRY(planarize<T>(at<T>(ws, p.o_lo), p.Q, p.n * p.d, at<T>(ws, p.o_loT), st));
             TRY(planarize<T>((const T*)queries, p.Q, p.n * p.d, at<T>(ws, p.o_qT), st));
-            TRY(planarize<T>((const T*)cands, p.N, p.n * p.d, at<T>(ws, p.o_candT), st));
+            if (!p.cand_planar) TRY(planarize<T>((const T*)cands, p.N, p.n * p.d, at<T>(ws, p.o_candT), st));
         }
         if (!EXACT) {
             const int DPq = (p.d + 1) / 2;
@@ -3485,8 +3494,8 @@ struct SearchImpl {
         tm.mark(1);
         if (p.has_lb)
             TRY((launch_lbmv_matrix<T, DMAX, EXACT>(at<T>(ws, p.o_upT), at<T>(ws, p.o_loT), at<T>(ws, p.o_qT),
-                                                    at<T>(ws, p.o_candT), p.Q, p.N, p.n, p.d, at<T>(ws, p.o_lb),
-                                                    at<T>(ws, p.o_ub), st, p.ub_stride)));
+                                                    candT, p.Q, p.N, p.n, p.d, at<T>(ws, p.o_lb),
+                                                    at<T>(ws, p.o_ub), st, p.ub_stride, false, p.ub_sampled)));
         if (p.rev) {
             // reverse LB_MV: the candidates' envelopes against the queries,
             // written transposed into the (query, candidate) layout

@@ -163,6 +163,8 @@ class SearchIndex:
         self.done_cap = 0  # completed-DTW list capacity (0 = library default; tests force 1)
         # thresholds frozen per DTW pass: run-to-run identical cell counts (work-model tuning)
         self.frozen_thresholds = False
+        self._planar = None  # planar copy of the collection for the LB_MV pass (built on first use)
+        self.cascade = True  # DTW also abandons on the LB_MV suffix (False: an A/B knob)
         self._ws = None
         self._ws_bytes = 0
         self._cenv = None  # (window, upper, lower): candidate-side index
@@ -192,6 +194,20 @@ class SearchIndex:
             self._cenv = (w, up, lo)
         return self._cenv[1], self._cenv[2]
 
+    def _planar_ptr(self, params: SearchParams, flags: int):
+        """The collection in the LB_MV pass's planar layout, made once per
+        index (tcdtw_planarize) instead of once per call; not for the
+        float32 filter on float64 data (its rounded copy is per call)."""
+        if params.method == Method.NONE or (flags & _lib.FLAG_F32_FILTER) or not _dev.torch().cuda.is_available():
+            return None
+        if self._planar is None:
+            N, n, d = self.candidates.shape
+            planar = _dev.torch().empty((n * d, N), dtype=self.tdtype, device=self.candidates.device)
+            _lib.check(_lib.lib().tcdtw_planarize(_lib.dtype_code(self.dtype), self.candidates.data_ptr(), N, n, d,
+                                                  planar.data_ptr(), _lib.stream_ptr()), "planarize")
+            self._planar = planar
+        return self._planar.data_ptr()
+
     def _filtering(self, reverse_bound: bool) -> bool:
         return self.f32_filter and not reverse_bound
 
@@ -206,6 +222,8 @@ class SearchIndex:
         flags = _lib.FLAG_TIMING if timing else 0
         if self.frozen_thresholds:
             flags |= _lib.FLAG_FROZEN_THRESHOLDS
+        if not self.cascade:
+            flags |= _lib.FLAG_NO_CASCADE
         rev = reverse_bound and params.method != Method.NONE
         if self._filtering(rev):
             flags |= _lib.FLAG_F32_FILTER
@@ -222,7 +240,8 @@ class SearchIndex:
             trigger_pc=params.trigger_pc, min_cell_frac=params.min_cell_frac, n_queries=n_q,
             n_candidates=self.n_candidates, candidate_base=self.base, seeds=seeds,
             flags=flags, phase_ms=ctypes.cast(phase_buf, ctypes.POINTER(ctypes.c_float)) if timing else None,
-            cand_upper=_lib.ptr(cu), cand_lower=_lib.ptr(cl), done_cap=self.done_cap)
+            cand_upper=_lib.ptr(cu), cand_lower=_lib.ptr(cl), done_cap=self.done_cap,
+            cand_planar=self._planar_ptr(params, flags))
 
     def workspace_bytes(self, params: SearchParams, advanced=None, n_q: int = 1, seeds: int = 0,
                         reverse_bound: bool = False) -> int:
@@ -270,6 +289,7 @@ class SearchIndex:
         self._ws = None
         self._ws_bytes = 0
         self._cenv = None
+        self._planar = None
 
     def prepare_queries(self, queries):
         t = _dev.torch()
