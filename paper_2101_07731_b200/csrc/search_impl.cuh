@@ -1633,7 +1633,10 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     // a head batch starts (heads) or fresh pairs start at row 0 (no heads).
     auto refill = [&]() {
         unsigned freem = __ballot_sync(FULL, !busy);
-        if (__popc(freem) < a.refill_min && freem != FULL) return;
+        if (freem == 0) return;
+        // queued pairs go to any free lane at once (a pop is a few loads); fresh
+        // tile entries wait until refill_min lanes are free
+        if (q_mask == 0 && __popc(freem) < a.refill_min && freem != FULL) return;
         while (freem) {
             if (q_mask) {  // pop: the rank-th free lane takes the rank-th queued slot
                 const int take = min(__popc(q_mask), __popc(freem));
