@@ -207,13 +207,26 @@ def index_envelope_stats(index, w, _lib, reps=5):
 
 
 # -------------------------------------------------------- CPU (oracle) legs
-def cpu_queries_per_sec(wl, w, method, advanced, n_queries_hint, budget_s, threads=0):
+def host_cpu() -> str:
+    """The host CPU model (lscpu's "Model name", from /proc/cpuinfo)."""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def cpu_queries_per_sec(wl, w, method, advanced, n_queries_hint, budget_s, threads=0, knobs=None):
     """Time the C port of the reference algorithm (oracle/, all threads) on
     a bounded sample of the queries against the full collection."""
     from oracle import oracle as O
 
     cands64 = wl.candidates.astype(np.float64)
-    params = O.make_params(w, method)
+    params = O.make_params(w, method, **(knobs or {}))
     threads = threads or (os.cpu_count() or 1)
     # one probe query on one thread to size the sample
     t0 = time.perf_counter()
@@ -228,10 +241,25 @@ def cpu_queries_per_sec(wl, w, method, advanced, n_queries_hint, budget_s, threa
     _, used = O.nn_search_batch(qs, cands64, params, advanced, wl.dim_range, n_threads=threads)
     wall = time.perf_counter() - t0
     return {"value": len(qs) / wall, "unit": "queries/s", "cores": int(used), "kind": "port",
+            "host_cpu": host_cpu(),
             "sample": f"{len(qs)} queries x {len(wl.candidates)} candidates, method {method}"
                       f"{'/' + advanced if advanced else ''}, W={w}, C port of mvdtw.nn_search "
                       f"(oracle/tcdtw_oracle.c), OpenMP over queries",
             "wall_s": wall}
+
+
+def cpu_tc_dtw(wl, w, budget_s):
+    """the CPU path also timed for tc_dtw, resolved as
+    the reference CLI does (cli.py:228-235: tune_params + tc_dtw_select on the
+    seeded sample, work model; untimed), then searched on a bounded sample."""
+    from oracle import oracle as O
+
+    e_ti, e_pc, lv, adv = O.resolve_tc_dtw(wl.queries.astype(np.float64), wl.candidates.astype(np.float64), w,
+                                           wl.dim_range, seed=42)
+    out = cpu_queries_per_sec(wl, w, "tc_dtw", adv, 0, budget_s,
+                              knobs={"trigger_ti": e_ti, "trigger_pc": e_pc, "quant_levels": lv})
+    out["resolved"] = {"advanced": adv, "trigger_ti": e_ti, "trigger_pc": e_pc, "quant_levels": lv}
+    return out
 
 
 # ----------------------------------------------------------------- main arms
@@ -268,16 +296,17 @@ def run_reference(args):
 
     wl = make_workload(args.config, n_candidates=args.candidates or None, n_queries=args.queries or None)
     w = wl.spec.windows()[args.window_index]
-    method, advanced = args.method, None
+    method, advanced, knobs = args.method, None, {}
     if method == "auto":  # the reference has no GPU-cost choice: its classic bound
         method = "lb_mv"
-    if method == "tc_dtw":
-        advanced = os.environ.get("TCDTW_REF_ADVANCED", "lb_pc")  # the GPU arm's tc_dtw_select pick on C4
     del core
     from oracle import oracle as O
 
     cands64 = wl.candidates.astype(np.float64)
-    params = O.make_params(w, method)
+    if method == "tc_dtw":  # resolved as the reference CLI does (cli.py:228-235), untimed
+        e_ti, e_pc, lv, advanced = O.resolve_tc_dtw(wl.queries.astype(np.float64), cands64, w, wl.dim_range, seed=42)
+        knobs = {"trigger_ti": e_ti, "trigger_pc": e_pc, "quant_levels": lv}
+    params = O.make_params(w, method, **knobs)
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
     O.nn_search_batch(wl.queries[:1].astype(np.float64), cands64, params, advanced, wl.dim_range, n_threads=1)
@@ -300,7 +329,7 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8d)",
         "config": {"workload": args.config, "n_candidates": len(wl.candidates), "n_queries_per_step": nq,
                    "window": w, "method": method, "advanced": advanced},
-        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "port", "host_cpu": host_cpu(),
                          "sample": f"{nq} queries/step x {len(wl.candidates)} candidates (C port of "
                                    f"mvdtw.nn_search, oracle/; single-query probe {per_query:.2f}s)"},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -468,6 +497,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         adv_name = None if advanced is None else advanced.value
         cpu = cpu_queries_per_sec(wl, w, params.method.value, adv_name, 0, args.cpu_seconds)
+        if params.method.value != "tc_dtw":
+            cpu["tc_dtw"] = cpu_tc_dtw(wl, w, args.cpu_seconds)
 
     if rank == 0:
         q_bytes = Qhost.numel() * Qhost.element_size()

@@ -287,5 +287,46 @@ def dtw_rows(queries, candidates, window, n_threads=0) -> np.ndarray:
     return out
 
 
+# --- the reference CLI's TC-DTW setup stage on the CPU (cli.py:228-235) ---------
+# tune_params (search.py:220-272) and tc_dtw_select (search.py:198-217) with the
+# reference's deterministic work model, costs from this oracle's nn_search.
+TUNE_CANDIDATE_SAMPLE, TUNE_QUERY_SAMPLE = 23, 8
+GRIDS = {"trigger_ti": (0.05, 0.1, 0.2), "trigger_pc": (0.1, 0.5), "quant_levels": (2, 3)}
+
+
+def _draw(items, size, rng):
+    """search.py:183-187: seeded subset in the original order."""
+    if len(items) <= size:
+        return np.asarray(items)
+    keep = np.sort(rng.choice(len(items), size=size, replace=False))
+    return np.asarray(items)[keep]
+
+
+def _work(queries, candidates, window, method, advanced, dim_range, **knobs) -> float:
+    outs, _ = nn_search_batch(queries, candidates, make_params(window, method, **knobs), advanced, dim_range)
+    return float(sum(o.work for o in outs))
+
+
+def resolve_tc_dtw(queries, candidates, window, dim_range=None, seed=42):
+    """(trigger_ti, trigger_pc, quant_levels, advanced) as the reference CLI
+    resolves method tc_dtw: the grid search on the seeded sample, then the
+    cheaper of LB_TI / LB_PC (ties to LB_PC)."""
+    rng = np.random.default_rng(seed)
+    sq = _draw(queries, TUNE_QUERY_SAMPLE, rng)
+    sc = _draw(candidates, TUNE_CANDIDATE_SAMPLE, rng)
+    ti_costs = [_work(sq, sc, window, "lb_ti", None, dim_range, trigger_ti=e) for e in GRIDS["trigger_ti"]]
+    e_ti = GRIDS["trigger_ti"][int(np.argmin(ti_costs))]
+    pc_grid = [(e, lv) for e in GRIDS["trigger_pc"] for lv in GRIDS["quant_levels"]]
+    pc_costs = [_work(sq, sc, window, "lb_pc", None, dim_range, trigger_pc=e, quant_levels=lv) for e, lv in pc_grid]
+    e_pc, lv = pc_grid[int(np.argmin(pc_costs))]
+    rng = np.random.default_rng(seed)
+    sq = _draw(queries, TUNE_QUERY_SAMPLE, rng)
+    sc = _draw(candidates, TUNE_CANDIDATE_SAMPLE, rng)
+    knobs = dict(trigger_ti=e_ti, trigger_pc=e_pc, quant_levels=lv)
+    cost_ti = _work(sq, sc, window, "lb_ti", None, dim_range, **knobs)
+    cost_pc = _work(sq, sc, window, "lb_pc", None, dim_range, **knobs)
+    return e_ti, e_pc, lv, ("lb_ti" if cost_ti < cost_pc else "lb_pc")
+
+
 def threads_available() -> int:
     return os.cpu_count() or 1
