@@ -484,6 +484,19 @@ def run_ours(args):
         roof = {"kernel": index.dtw_kernel(params, advanced, batch), "bound": "alu", "achieved": achieved, "peak": alu_peak,
                 "unit": "Tlane-op/s", "frac": achieved / alu_peak, "traffic": traffic_from_profile(dtw_cells / max(1, -(-n_q // batch))),
                 "algorithmic_ops": f"(2d+4) = {2 * d + 4} per DP cell x {dtw_cells:.4g} cells (SURVEY 8d)"}
+    if ph.get("advanced", 0.0) > 0 and ctr.get("advanced_lb_evals", 0) > 0 and advanced is not None:
+        # the second-stage bound's kernel against the same ALU roof, SURVEY 8(d) op counts per evaluated pair
+        a_name = getattr(advanced, "value", str(advanced))
+        if a_name == "lb_pc":
+            per_pair = n * (5 * params.max_boxes * d + params.max_boxes + 2)
+        else:  # lb_ti
+            per_pair = n * ((2 * w + 1) * 10 + 2 * d + (2 * w + 1) * (2 * d + 1) / params.refresh_period)
+        a_ach = ctr["advanced_lb_evals"] * per_pair / (ph["advanced"] / 1e3) / 1e12
+        roof["advanced"] = {"kernel": "advanced_pc_kernel" if a_name == "lb_pc" else "advanced_kernel (LB_TI)",
+                            "bound": "alu", "achieved": a_ach, "peak": alu_peak, "frac": a_ach / alu_peak,
+                            "ops_per_pair": per_pair, "pairs": ctr["advanced_lb_evals"], "ms": ph["advanced"],
+                            "note": "full-length op count; the cascade stops most pairs early, so frac "
+                                    "understates the kernel's issue rate"}
     lanes = 128 if dtw_f32 else 64
     nominal = 148 * lanes * measured_peaks().get("sm_max_mhz", 1965) / 1e6
     roof["peak_source"] = (f"tcdtw_alu_probe {'FFMA' if dtw_f32 else 'DFMA'} issue rate measured in this "

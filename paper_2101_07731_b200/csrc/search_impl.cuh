@@ -2277,6 +2277,51 @@ __global__ void __launch_bounds__(256, 2) dtw_wave_d_kernel(SArgs<T> a, Tiles tl
 // reference points (the 2W+1 slots) and the column minima; with `ring_smem`
 // those rings live in the warp's shared memory (lane-interleaved, conflict
 // free) instead of global scratch.
+// The LB_MV suffix cascade of the second-stage bounds.  LB_PC, LB_TI and
+// LB_AD, like LB_MV, add one nonnegative floor per candidate point, each a
+// lower bound of the cheapest window cell that point's DTW row can use; so
+// sum_t max(adv_t, mv_t) is a lower bound too, and with the points not yet
+// reached bounded by the LB_MV suffix (LB_MV total - LB_MV prefix, the slack
+// of the DTW cascade) a pair is dropped as soon as
+//   sum_{t < next} max(adv_t, mv_t) + suffix > threshold.
+// It only ever prunes more than the reference's bound alone (search.py:163):
+// the answers do not change.
+template <typename T, int DMAX, bool EXACT>
+__device__ __forceinline__ T mv_point(const T (&cp)[DMAX], const T* __restrict__ u, const T* __restrict__ l, int d) {
+    if constexpr (EXACT) {
+        return lbmv_term_exact<T, DMAX>(cp, u, l, d);
+    } else {
+        T s = T(0);
+#pragma unroll
+        for (int p = 0; p < DMAX; ++p)
+            if (p < d) {
+                const T dv = tmax(tmax(cp[p] - u[p], l[p] - cp[p]), T(0));
+                s = fma(dv, dv, s);
+            }
+        return fast_sqrt(s);
+    }
+}
+
+template <typename T, bool EXACT>
+struct AdvCascade {
+    bool on;
+    T lbtot, comb = T(0), mv = T(0);
+    __device__ __forceinline__ void add(T adv_t, T mv_t) {
+        const T m = adv_t > mv_t ? adv_t : mv_t;
+        comb = EXACT ? add_rn(comb, m) : comb + m;
+        mv = EXACT ? add_rn(mv, mv_t) : mv + mv_t;
+    }
+    // lower bound of the DTW from the points so far plus the LB_MV suffix
+    __device__ __forceinline__ T bound(const SArgs<T>& a) const {
+        if (!on) return comb;
+        const T suf = lbtot * a.casc_lo - mv * a.casc_hi;
+        return comb + (suf > T(0) ? suf : T(0));
+    }
+    __device__ __forceinline__ bool over(const SArgs<T>& a, T thr) const {
+        return on ? bound(a) > thr * a.casc_thr : comb > thr;
+    }
+};
+
 template <typename T, int DMAX, bool EXACT>
 __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int64_t n_tiles,
                                                        const uint32_t* __restrict__ cand_of, T* __restrict__ res,
@@ -2306,11 +2351,14 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
                                 : (lb1 > a.trigger * db));
         const T* qa = a.queries + q * (int64_t)n * d;
         const T* ca = a.cands + c * (int64_t)n * d;
+        const T* eu = a.env_up ? a.env_up + q * (int64_t)n * d : nullptr;
+        const T* el = a.env_lo ? a.env_lo + q * (int64_t)n * d : nullptr;
+        AdvCascade<T, EXACT> cas{a.cascade && eu != nullptr, lb1};
         T val = T(0);
         if (a.adv == TCDTW_METHOD_LB_PC) {
             const T* bl = a.box_lo + q * (int64_t)a.G * a.K * d;
             const T* bh = a.box_hi + q * (int64_t)a.G * a.K * d;
-            for (int t = 0; t < n && __any_sync(0xffffffffu, go && val <= thr); ++t) {
+            for (int t = 0; t < n && __any_sync(0xffffffffu, go && !cas.over(a, thr)); ++t) {
                 T cp[DMAX];
                 load_point<T, DMAX>(cp, ca + (int64_t)t * d, d);
                 const int g = t / a.gw;
@@ -2332,10 +2380,12 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
                     }
                     best = tmin(best, v2);
                 }
-                val = EXACT ? add_rn(val, sqrt_rn(best)) : val + fast_sqrt(best);
+                const T pc_t = EXACT ? sqrt_rn(best) : fast_sqrt(best);
+                cas.add(pc_t, cas.on ? mv_point<T, DMAX, EXACT>(cp, eu + (int64_t)t * d, el + (int64_t)t * d, d) : T(0));
             }
+            val = cas.bound(a);
         } else if (a.adv == TCDTW_METHOD_LB_AD) {
-            for (int t = 0; t < n && __any_sync(0xffffffffu, go && val <= thr); ++t) {
+            for (int t = 0; t < n && __any_sync(0xffffffffu, go && !cas.over(a, thr)); ++t) {
                 T cp[DMAX];
                 load_point<T, DMAX>(cp, ca + (int64_t)t * d, d);
                 const int lo = t - w < 0 ? 0 : t - w;
@@ -2357,8 +2407,9 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
                     }
                     m = tmin(m, dj);
                 }
-                val = EXACT ? add_rn(val, m) : val + m;
+                cas.add(m, cas.on ? mv_point<T, DMAX, EXACT>(cp, eu + (int64_t)t * d, el + (int64_t)t * d, d) : T(0));
             }
+            val = cas.bound(a);
         } else {
             // LB_TI, TIP_TOP variant (search.py:150-153), lb_ti.py:140-200.
             // Slot rings of size B per lane, interleaved by lane in scratch.
@@ -2437,9 +2488,15 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
                     }
                     while (next_final <= i - w) {
                         const T cmv = cm_r[(next_final % B) * 32 + lane];
-                        val = EXACT ? add_rn(val, cmv) : val + cmv;
+                        T mvj = T(0);
+                        if (cas.on) {
+                            T cp[DMAX];
+                            load_point<T, DMAX>(cp, ca + (int64_t)next_final * d, d);
+                            mvj = mv_point<T, DMAX, EXACT>(cp, eu + (int64_t)next_final * d, el + (int64_t)next_final * d, d);
+                        }
+                        cas.add(cmv, mvj);
                         ++next_final;
-                        if (val > thr) { stop = true; break; }
+                        if (cas.over(a, thr)) { stop = true; break; }
                     }
                 }
                 prev_lo = lo;
@@ -2448,12 +2505,19 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
             if (!stop) {
                 while (next_final < n) {
                     const T cmv = cm_r[(next_final % B) * 32 + lane];
-                    val = EXACT ? add_rn(val, cmv) : val + cmv;
+                    T mvj = T(0);
+                    if (cas.on) {
+                        T cp[DMAX];
+                        load_point<T, DMAX>(cp, ca + (int64_t)next_final * d, d);
+                        mvj = mv_point<T, DMAX, EXACT>(cp, eu + (int64_t)next_final * d, el + (int64_t)next_final * d, d);
+                    }
+                    cas.add(cmv, mvj);
                     ++next_final;
                 }
             }
+            val = cas.bound(a);
         }
-        if (go && val > thr) res[ent] = T(-1);
+        if (go && (cas.on ? val > thr * a.casc_thr : val > thr)) res[ent] = T(-1);
         int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
         warp_add_counter(ctr + TCDTW_C_ADVANCED_LB_EVALS, go ? 1 : 0);
     }
@@ -2502,9 +2566,11 @@ __global__ void __launch_bounds__(256) advanced_pc_kernel(SArgs<T> a, Tiles tl, 
         const bool go = has && !(res[ent] < T(0)) && (lb1 > a.trigger * db);  // trigger band, search.py:147
         const T* crow = a.cands + c * (int64_t)n * D;
         using PL = PairLoad<T, D>;
-        T val = T(0);
+        const T* eu = a.env_up ? a.env_up + q * (int64_t)n * D : nullptr;
+        const T* el = a.env_lo ? a.env_lo + q * (int64_t)n * D : nullptr;
+        AdvCascade<T, sizeof(T) == 8> cas{a.cascade && eu != nullptr, lb1};
         // two candidate rows per pass: one vectorised load of 2D values
-        for (int t = 0; t < n && __any_sync(FULL, go && val <= thr); t += 2) {
+        for (int t = 0; t < n && __any_sync(FULL, go && !cas.over(a, thr)); t += 2) {
             T cp2[2 * D];
             if (VEC && t + 1 < n) {
                 const typename PL::V* src = reinterpret_cast<const typename PL::V*>(crow + (int64_t)t * D);
@@ -2535,11 +2601,18 @@ __global__ void __launch_bounds__(256) advanced_pc_kernel(SArgs<T> a, Tiles tl, 
                         }
                         best = tmin(best, acc);
                     }
-                    val += fast_sqrt(best);
+                    T mv_t = T(0);
+                    if (cas.on) {
+                        T cpd[D];
+#pragma unroll
+                        for (int p = 0; p < D; ++p) cpd[p] = cp2[r * D + p];
+                        mv_t = mv_point<T, D, false>(cpd, eu + (int64_t)(t + r) * D, el + (int64_t)(t + r) * D, D);
+                    }
+                    cas.add(fast_sqrt(best), mv_t);
                 }
             }
         }
-        if (go && val > thr) res[ent] = T(-1);
+        if (go && cas.over(a, thr)) res[ent] = T(-1);
         int64_t* ctr = a.counters + q * TCDTW_COUNTERS;
         warp_add_counter(ctr + TCDTW_C_ADVANCED_LB_EVALS, go ? 1 : 0);
     }
