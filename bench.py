@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-exchange", action="store_true", help="skip the d_best all-reduce between phases")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (testing)")
     ap.add_argument("--no-cascade", action="store_true", help="A/B: DTW abandons on row minima only")
+    ap.add_argument("--reverse-pc", action="store_true",
+                    help="f2: with an LB_PC second stage, also prune on the reverse LB_PC (candidate box sets)")
     ap.add_argument("--reverse-bound", action="store_true",
                     help="also prune on LB_MV(q, env(c)) from the candidate-side index (SURVEY 8f f2)")
     return ap.parse_args()
@@ -389,7 +391,7 @@ def run_ours(args):
     def step(queries, to_host=False):
         res = index.search(queries, params, advanced=advanced, dim_range=wl.dim_range, batch=batch,
                            seeds=args.seeds, dbest_hook=hook, return_device=True,
-                           reverse_bound=args.reverse_bound)
+                           reverse_bound=args.reverse_bound, reverse_pc=args.reverse_pc)
         idx, dist_ = res.best_index, res.best_distance
         if world > 1:
             idx, dist_ = combine_results(idx, dist_, group)
@@ -435,7 +437,8 @@ def run_ours(args):
 
     # instrumented pass: phase times (CUDA events per phase), counters
     res = index.search(Qdev, params, advanced=advanced, dim_range=wl.dim_range, batch=batch, seeds=args.seeds,
-                       timing=True, dbest_hook=hook, return_device=True, reverse_bound=args.reverse_bound)
+                       timing=True, dbest_hook=hook, return_device=True, reverse_bound=args.reverse_bound,
+                       reverse_pc=args.reverse_pc)
     ph = res.phase_ms
     ctr = {k: v.sum().item() for k, v in res.counters.items()}
     if world > 1:
@@ -525,6 +528,7 @@ def run_ours(args):
                        "trigger_ti": params.trigger_ti, "trigger_pc": params.trigger_pc,
                        "quant_levels": params.quant_levels, "query_batch": batch,
                        "reverse_bound": bool(args.reverse_bound), "cascade": not args.no_cascade,
+                       "reverse_pc": bool(args.reverse_pc),
                        "parallelism": f"candidate shards x{world}",
                        "l2": "inputs larger than L2 (collection resident in HBM, no flush)"},
             "e2e": {"value": n_q / (e2e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": q_bytes,

@@ -168,6 +168,13 @@ typedef struct tcdtw_search_desc {
      * collection with tcdtw_planarize; NULL = planarised into the workspace
      * on every call.  Ignored with TCDTW_FLAG_F32_FILTER. */
     const void *cand_planar;
+    /* Candidate-side box sets (ABI version 3): every
+     * candidate's LB_PC boxes, (n_candidates, G, max_boxes, dims) lo / hi of
+     * `dtype`, +inf / -inf padded, built with tcdtw_build_box_sets using this
+     * search's window, group_width, quant_levels, max_boxes, min_cell_frac
+     * and dim_range.  Read only with TCDTW_FLAG_REVERSE_PC. */
+    const void *cand_box_lo;
+    const void *cand_box_hi;
 } tcdtw_search_desc;
 
 #define TCDTW_FLAG_TIMING 1     /* fill desc->phase_ms (synchronises the stream) */
@@ -191,6 +198,13 @@ typedef struct tcdtw_search_desc {
 /* DTW abandons on its row minima only, without the LB_MV suffix cascade
  * (an A/B knob: the same answers, more DP cells). */
 #define TCDTW_FLAG_NO_CASCADE 32
+/* With an LB_PC second stage, also bound every triggered pair by the reverse
+ * LB_PC -- the query's points against the candidate's box sets
+ * (desc->cand_box_lo/hi) -- and prune on the larger of the two.  DTW is
+ * symmetric in its arguments for equal lengths, so both are lower bounds
+ * (an extension; "switch the role").  Not combined with
+ * TCDTW_FLAG_F32_FILTER. */
+#define TCDTW_FLAG_REVERSE_PC 64
 #define TCDTW_PHASES 8      /* prep, lb_mv, seeds_topk, seeds_dtw, compact, advanced, dtw, finalize */
 #define TCDTW_COUNTERS 9    /* per query: see enum below */
 

@@ -28,6 +28,7 @@ FLAG_F32_FILTER = 4
 FLAG_DEBUG_SYNC = 8
 FLAG_FROZEN_THRESHOLDS = 16
 FLAG_NO_CASCADE = 32
+FLAG_REVERSE_PC = 64
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -48,7 +49,7 @@ class SearchDesc(ctypes.Structure):
         ("min_cell_frac", ctypes.c_double), ("n_queries", _i64), ("n_candidates", _i64),
         ("candidate_base", _i64), ("seeds", _i32), ("flags", _i32),
         ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("cand_upper", _vp), ("cand_lower", _vp),
-        ("done_cap", _i64), ("cand_planar", _vp),
+        ("done_cap", _i64), ("cand_planar", _vp), ("cand_box_lo", _vp), ("cand_box_hi", _vp),
     ]
 
 

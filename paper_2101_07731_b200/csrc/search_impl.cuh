@@ -721,6 +721,9 @@ struct SArgs {
     const double* xc;
     // R-row lane kernel: per-warp scratch of its head batches (nullptr: none)
     float* lane_scratch;
+    // reverse LB_PC: the candidates' box sets (N, G, K, d), nullptr = off
+    const T* cbox_lo;
+    const T* cbox_hi;
 };
 
 template <typename T>
@@ -2384,6 +2387,41 @@ __global__ void __launch_bounds__(256) advanced_kernel(SArgs<T> a, Tiles tl, int
                 cas.add(pc_t, cas.on ? mv_point<T, DMAX, EXACT>(cp, eu + (int64_t)t * d, el + (int64_t)t * d, d) : T(0));
             }
             val = cas.bound(a);
+            if (a.cbox_lo) {
+                // reverse LB_PC: the query's points against the candidate's
+                // boxes (its own expanded windows), for pairs the forward
+                // bound kept; prune on the larger of the two
+                const bool fwd_pruned = cas.on ? val > thr * a.casc_thr : val > thr;
+                const T* cl = a.cbox_lo + c * (int64_t)a.G * a.K * d;
+                const T* ch = a.cbox_hi + c * (int64_t)a.G * a.K * d;
+                T rv = T(0);
+                bool live = go && !fwd_pruned;
+                for (int t = 0; t < n && __any_sync(0xffffffffu, live && rv <= thr); ++t) {
+                    T qp[DMAX];
+                    load_point<T, DMAX>(qp, qa + (int64_t)t * d, d);
+                    const int g = t / a.gw;
+                    T best = INF;
+                    for (int k = 0; k < a.K; ++k) {
+                        const T* lo = cl + ((int64_t)g * a.K + k) * d;
+                        const T* hi = ch + ((int64_t)g * a.K + k) * d;
+                        T v2;
+                        if constexpr (EXACT) {
+                            v2 = boxdist2_exact<T, DMAX>(qp, lo, hi, d);
+                        } else {
+                            v2 = T(0);
+#pragma unroll
+                            for (int p = 0; p < DMAX; ++p)
+                                if (p < d) {
+                                    const T dv = tmax(tmax(lo[p] - qp[p], qp[p] - hi[p]), T(0));
+                                    v2 = fma(dv, dv, v2);
+                                }
+                        }
+                        best = tmin(best, v2);
+                    }
+                    rv = EXACT ? add_rn(rv, sqrt_rn(best)) : rv + fast_sqrt(best);
+                }
+                if (live && rv > thr) val = dev_inf<T>();  // pruned by the reverse bound
+            }
         } else if (a.adv == TCDTW_METHOD_LB_AD) {
             for (int t = 0; t < n && __any_sync(0xffffffffu, go && !cas.over(a, thr)); ++t) {
                 T cp[DMAX];
@@ -3129,6 +3167,7 @@ struct Plan {
     bool has_lb, exact, rev;
     bool f32f;  // TCDTW_FLAG_F32_FILTER: float64 inputs, float32 filter
     bool cand_planar;  // desc->cand_planar is used instead of o_candT
+    bool rev_pc;       // TCDTW_FLAG_REVERSE_PC with an LB_PC second stage
     size_t o_q32, o_c32, o_slack, o_lanesc, o_dbf;
     int64_t max_tiles;
     // byte offsets
@@ -3177,6 +3216,13 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     p.rev = p.has_lb && (dsc->flags & TCDTW_FLAG_REVERSE_LB) != 0;
     if (p.rev && (!dsc->cand_upper || !dsc->cand_lower)) return TCDTW_INVALID_INPUT;
     if (p.rev && p.f32f) return TCDTW_NOT_SUPPORTED;
+    {
+        const bool pc = dsc->method == TCDTW_METHOD_LB_PC ||
+                        (dsc->method == TCDTW_METHOD_TC_DTW && dsc->advanced == TCDTW_METHOD_LB_PC);
+        p.rev_pc = pc && (dsc->flags & TCDTW_FLAG_REVERSE_PC) != 0;
+        if (p.rev_pc && (!dsc->cand_box_lo || !dsc->cand_box_hi)) return TCDTW_INVALID_INPUT;
+        if (p.rev_pc && p.f32f) return TCDTW_NOT_SUPPORTED;
+    }
     p.S = p.has_lb ? (dsc->seeds > 0 ? dsc->seeds : 8) : 0;
     if (p.S > kSeedMax) return TCDTW_INVALID_INPUT;
     if (p.S > p.N) p.S = (int)p.N;
@@ -3375,6 +3421,8 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
     a.mg.add = nullptr;
     a.xq = a.xc = nullptr;
     a.lane_scratch = (!p.exact && laner_rows_shape(p.n, p.d, p.B) > 0) ? at<float>(ws, p.o_lanesc) : nullptr;
+    a.cbox_lo = p.rev_pc ? (const T*)dsc->cand_box_lo : nullptr;
+    a.cbox_hi = p.rev_pc ? (const T*)dsc->cand_box_hi : nullptr;
     if (p.f32f) {  // queries / cands are the float32 copies in the workspace
         a.queries = at<T>(ws, p.o_q32);
         a.cands = at<T>(ws, p.o_c32);
@@ -3685,7 +3733,7 @@ struct SearchImpl {
         tm.mark(5);
         if (a.adv >= 0) {
             int sa = TCDTW_NOT_SUPPORTED;
-            if (a.adv == TCDTW_METHOD_LB_PC)
+            if (a.adv == TCDTW_METHOD_LB_PC && !p.rev_pc)
                 sa = launch_advanced_pc<T>(a, p.d, tl, n_tiles, surv, res, at<int>(ws, p.o_tctr), st);
             if (sa == TCDTW_NOT_SUPPORTED) {
                 cudaMemsetAsync(at<int>(ws, p.o_tctr), 0, sizeof(int), st);

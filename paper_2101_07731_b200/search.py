@@ -165,6 +165,10 @@ class SearchIndex:
         self.frozen_thresholds = False
         self._planar = None  # planar copy of the collection for the LB_MV pass (built on first use)
         self.cascade = True  # DTW also abandons on the LB_MV suffix (False: an A/B knob)
+        self._cbox = None  # candidate box sets (f2), per parameter key
+        self._csteps = None  # candidate neighbour steps (f2)
+        self._reverse_pc = False  # the current search uses the reverse LB_PC (set by search())
+        self._reverse_pc_range = None
         self._ws = None
         self._ws_bytes = 0
         self._cenv = None  # (window, upper, lower): candidate-side index
@@ -209,12 +213,41 @@ class SearchIndex:
         return self._planar.data_ptr()
 
     def _filtering(self, reverse_bound: bool) -> bool:
-        return self.f32_filter and not reverse_bound
+        return self.f32_filter and not reverse_bound and not self._reverse_pc
 
     def work_tdtype(self, reverse_bound: bool = False):
         """Element type of d_best and dim_range: float32 under the filter."""
         t = _dev.torch()
         return t.float32 if self._filtering(reverse_bound) else self.tdtype
+
+    def candidate_box_sets(self, params: SearchParams, dim_range=None):
+        """Candidate-side index: every candidate's LB_PC
+        box sets (lb_pc.py:239-261 applied to the collection), built once per
+        (window, group width, levels, boxes, cell fraction, dim_range) and
+        kept resident: (lo, hi, counts) with shapes (N, G, K, D) and (N, G).
+        They enable the reverse LB_PC (``search(..., reverse_pc=True)``)."""
+        from .lb_pc import build_box_sets_batch
+
+        n = int(self.candidates.shape[1])
+        key = (min(int(params.window), n - 1), params.group_width, params.quant_levels, params.max_boxes,
+               float(params.min_cell_frac), None if dim_range is None else tuple(np.asarray(dim_range).ravel().tolist()))
+        if self._cbox is None or self._cbox[0] != key:
+            self._cbox = None
+            lo, hi, cnt = build_box_sets_batch(self.candidates, key[0], params.group_width, params.quant_levels,
+                                               params.max_boxes, params.min_cell_frac, dim_range, self.tdtype)
+            self._cbox = (key, lo, hi, cnt)
+        return self._cbox[1], self._cbox[2], self._cbox[3]
+
+    def candidate_steps(self):
+        """Candidate-side index (f2): every candidate's neighbour steps
+        d(c_{t-1}, c_t) (lb_ti.py:51-55), shape (N, n-1), built once; the
+        BASIC / TIP variants of LB_TI take them as candidate steps
+        (NeighborDistances, lb_ti.py:58-76)."""
+        from .lb_ti import neighbor_steps_batch
+
+        if self._csteps is None:
+            self._csteps = neighbor_steps_batch(self.candidates, self.tdtype)
+        return self._csteps
 
     def _desc(self, params: SearchParams, adv: Method | None, n_q: int, seeds: int, timing: bool,
               phase_buf, reverse_bound: bool = False) -> _lib.SearchDesc:
@@ -231,6 +264,11 @@ class SearchIndex:
         if rev:
             cu, cl = self.candidate_envelopes(params.window)
             flags |= _lib.FLAG_REVERSE_LB
+        cbl = cbh = None
+        uses_pc = params.method == Method.LB_PC or (params.method == Method.TC_DTW and adv == Method.LB_PC)
+        if self._reverse_pc and uses_pc:
+            cbl, cbh, _ = self.candidate_box_sets(params, self._reverse_pc_range)
+            flags |= _lib.FLAG_REVERSE_PC
         return _lib.SearchDesc(
             dtype=_lib.dtype_code(self.dtype), n=n, dims=d, window=int(params.window),
             method=METHOD_CODE[params.method],
@@ -241,7 +279,7 @@ class SearchIndex:
             n_candidates=self.n_candidates, candidate_base=self.base, seeds=seeds,
             flags=flags, phase_ms=ctypes.cast(phase_buf, ctypes.POINTER(ctypes.c_float)) if timing else None,
             cand_upper=_lib.ptr(cu), cand_lower=_lib.ptr(cl), done_cap=self.done_cap,
-            cand_planar=self._planar_ptr(params, flags))
+            cand_planar=self._planar_ptr(params, flags), cand_box_lo=_lib.ptr(cbl), cand_box_hi=_lib.ptr(cbh))
 
     def workspace_bytes(self, params: SearchParams, advanced=None, n_q: int = 1, seeds: int = 0,
                         reverse_bound: bool = False) -> int:
@@ -290,6 +328,8 @@ class SearchIndex:
         self._ws_bytes = 0
         self._cenv = None
         self._planar = None
+        self._cbox = None
+        self._csteps = None
 
     def prepare_queries(self, queries):
         t = _dev.torch()
@@ -351,7 +391,21 @@ class SearchIndex:
 
     def search(self, queries, params: SearchParams, advanced=None, dim_range=None, batch: int | None = None,
                seeds: int = 0, timing: bool = False, dbest_hook=None, return_device: bool = False,
-               reverse_bound: bool = False) -> BatchOutcome:
+               reverse_bound: bool = False, reverse_pc: bool = False) -> BatchOutcome:
+        """1-NN of every query (see _search).  reverse_pc=True (with an LB_PC
+        second stage) also prunes on the reverse LB_PC against the
+        candidates' own box sets (candidate_box_sets); the answers are the
+        same, only the counters change."""
+        self._reverse_pc, self._reverse_pc_range = bool(reverse_pc), dim_range
+        try:
+            return self._search(queries, params, advanced, dim_range, batch, seeds, timing, dbest_hook,
+                                return_device, reverse_bound)
+        finally:
+            self._reverse_pc, self._reverse_pc_range = False, None
+
+    def _search(self, queries, params: SearchParams, advanced=None, dim_range=None, batch: int | None = None,
+                seeds: int = 0, timing: bool = False, dbest_hook=None, return_device: bool = False,
+                reverse_bound: bool = False) -> BatchOutcome:
         """1-NN of every query.  `dbest_hook(d_best_tensor)` (optional) may
         tighten the per-query best-so-far between the two phases, e.g. an
         NCCL min-allreduce across shards.  With return_device=True the
