@@ -45,7 +45,7 @@ using namespace tcdtw;
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static inline bool dtype_ok(int t) { return t == TCDTW_F32 || t == TCDTW_F64; }
 static inline bool shape_ok(int64_t count, int32_t n, int32_t dims) {
-    return count >= 0 && n >= 1 && dims >= 1 && dims <= kMaxDims;
+    return count >= 0 && n >= 1 && dims >= 1;
 }
 static inline int eff_window(int32_t window, int32_t n) { return window < n - 1 ? window : n - 1; }
 

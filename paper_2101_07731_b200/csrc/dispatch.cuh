@@ -22,7 +22,7 @@ int dispatch_dims(int dims, F&& f, Args&&... args) {
     if (dims <= DM) return f.template run<T, DM>(args...);
     TCDTW_DIMS_BUCKETS(TCDTW_CASE)
 #undef TCDTW_CASE
-    return TCDTW_INVALID_INPUT;
+    return TCDTW_NOT_SUPPORTED;  // a valid input the register buckets do not cover
 }
 
 template <typename F, typename... Args>

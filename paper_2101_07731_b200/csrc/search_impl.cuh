@@ -3187,7 +3187,8 @@ static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     if (!dsc) return TCDTW_INVALID_INPUT;
     if (dsc->dtype != TCDTW_F32 && dsc->dtype != TCDTW_F64) return TCDTW_INVALID_INPUT;
-    if (dsc->n < 1 || dsc->dims < 1 || dsc->dims > kMaxDims || dsc->window < 0) return TCDTW_INVALID_INPUT;
+    if (dsc->n < 1 || dsc->dims < 1 || dsc->window < 0) return TCDTW_INVALID_INPUT;
+    if (dsc->dims > 32) return TCDTW_NOT_SUPPORTED;  // the search's register buckets stop at 32 dimensions
     if (dsc->n_queries < 1 || dsc->n_queries > 65535 || dsc->n_candidates < 1 || dsc->n_candidates > 0xfffffff0LL)
         return TCDTW_INVALID_INPUT;  // queries per call: one compaction grid row each
     if (dsc->method < TCDTW_METHOD_NONE || dsc->method > TCDTW_METHOD_LB_AD) return TCDTW_INVALID_INPUT;

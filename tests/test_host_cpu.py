@@ -67,6 +67,23 @@ def test_workspace_size_and_validation_without_gpu():
     assert L.tcdtw_build_box_sets(1, None, 1, 4, 3, 1, 0, 2, 6, 1e-5, None, None, None, None, None) == 1
 
 
+def test_unsupported_dims_are_not_invalid_input():
+    """a valid input beyond the kernels' dimension buckets is
+    TCDTW_NOT_SUPPORTED (TcdtwError), not InvalidInputError."""
+    import ctypes
+
+    from paper_2101_07731_b200 import _lib
+
+    L = _lib.load_library()
+    d = _lib.SearchDesc(dtype=0, n=64, dims=61, window=6, method=1, advanced=0, refresh_period=5, quant_levels=2,
+                        max_boxes=6, group_width=6, trigger_ti=0.1, trigger_pc=0.1, min_cell_frac=1e-5,
+                        n_queries=4, n_candidates=100, candidate_base=0, seeds=0, flags=0)
+    out = ctypes.c_size_t()
+    assert L.tcdtw_search_workspace_size(ctypes.byref(d), ctypes.byref(out)) == _lib.TCDTW_NOT_SUPPORTED
+    with pytest.raises(_lib.TcdtwError):
+        _lib.check(_lib.TCDTW_NOT_SUPPORTED, "search")
+
+
 def test_search_params_validation():
     from paper_2101_07731_b200 import InvalidInputError, Method, SearchParams
 
