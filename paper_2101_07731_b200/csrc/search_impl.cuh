@@ -1647,6 +1647,10 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                 const int sl = (int)__fns(q_mask, 0, (rank < take ? rank : 0) + 1);
                 const uint32_t cs = __shfl_sync(FULL, q_cand, sl);
                 if (!busy && rank < take) {
+                    if (slot_q != cq) {  // the lane's last pair may belong to the previous query
+                        flush();
+                        cq = slot_q;
+                    }
                     ent = q_base + sl;
                     cand = cs;
                     lbtot = q_lb[sl];

@@ -464,3 +464,25 @@ def test_select_method_gpu_cost(P):
         ref = P.nn_search(q, cands, P.SearchParams(window=5, method="none"))
         out = P.nn_search(q, cands, params, advanced=adv)
         assert (out.best_index, out.best_distance) == (ref.best_index, ref.best_distance)
+
+
+@pytest.mark.parametrize("method", ["lb_pc", "lb_mv"])
+def test_lane_kernel_query_switches_are_attributed(P, method):
+    """The R-row lane kernel with head batches switches queries many times
+    per warp; with LB_PC pruning most entries, head batches are sparse and
+    lanes pop queued pairs they did not start (a lane's query attribution
+    must follow the pair: a stale one put completed DTWs on the wrong query,
+    round-2 bug).  C4 shape, 16 queries x 100k candidates, three runs, every
+    answer == the oracle."""
+    from oracle import oracle as O
+    from paper_2101_07731_b200.datasets import make_workload
+
+    wl = make_workload("C4", n_candidates=100_000, n_queries=16)
+    outs, _ = O.nn_search_batch(wl.queries.astype(np.float64), wl.candidates.astype(np.float64),
+                                O.make_params(12, method), None, wl.dim_range)
+    index = P.SearchIndex(wl.candidates, dtype="f32")
+    assert index.dtw_kernel(_params(P, 12, method), None, 16).startswith("dtw_laner")
+    for _ in range(3):
+        res = index.search(wl.queries, _params(P, 12, method), dim_range=wl.dim_range)
+        assert res.best_index.tolist() == [o.best_index for o in outs]
+        assert res.best_distance.tolist() == [o.best_distance for o in outs]
