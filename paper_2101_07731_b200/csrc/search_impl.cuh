@@ -1478,9 +1478,8 @@ struct LaneRLayout {
     __host__ __device__ static int warp_words(int n, int qrows, int B) { return q_words(qrows) + e_words(n) + B * 32; }
 };
 
-// Per-warp global scratch of the lane kernel's head batches: the parked
-// body state (band rows + scalars) and the queued pairs' band rows,
-// lane-interleaved (coalesced).
+// Per-warp global scratch of the lane kernel's head batches: the queued
+// pairs' band rows and scalars, lane-interleaved (coalesced).
 __host__ __device__ inline int laner_scratch_words(int B) { return 2 * B * 32 + 9 * 32; }
 constexpr int kLanerMaxWarps = 148 * 32;
 
@@ -1509,52 +1508,51 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     float* const ps = es + L::e_words(n) + lane;                           // band row: slot k at ps[k*32]
     const unsigned FULL = 0xffffffffu;
     const float INF = dev_inf<float>();
+    const int thr_mask = a.thr_every - 1;
     const bool casc = CASC && a.lb != nullptr && a.abandon && a.env_up != nullptr && a.cascade;
     const bool heads = HS > 0 && n > R * (HS + 1) && a.lane_scratch != nullptr;
     float* const scr = a.lane_scratch + (size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * laner_scratch_words(B);
-    float* const park_band = scr + lane;
-    float* const queue_band = scr + 32 * B;
-    int* const park_i = reinterpret_cast<int*>(scr + 64 * B);
-    int* const park_el = park_i + 32;
-    int* const park_eh = park_i + 64;
-    uint32_t* const park_c = reinterpret_cast<uint32_t*>(park_i + 96);
-    float* const park_lb = scr + 64 * B + 128;
-    float* const park_pre = scr + 64 * B + 160;
-    int* const park_busy = park_i + 192;
-    // queued pairs (slot = the head lane that ran them): band row, LB_MV
-    // total and cascade prefix in scratch; the candidate stays in that lane's
-    // register q_cand (the pop's row loads depend on it)
-    float* const q_lb = scr + 64 * B + 224;
+    // queued pairs (slot = the lane that ran them): band row, result entry,
+    // LB_MV total and cascade prefix in scratch; the candidate and the next
+    // row stay in that lane's registers q_cand / q_i (the pop's row loads
+    // depend on them)
+    float* const q_band = scr;
+    int* const q_el = reinterpret_cast<int*>(scr + 32 * B);
+    int* const q_eh = q_el + 32;
+    float* const q_lb = scr + 32 * B + 64;
+    float* const q_pre = scr + 32 * B + 96;
     // warp-uniform work state: current tile, reservoir window, query in smem
     int64_t t_begin = 0;
     int t_q = -1, t_len = 0, t_next = 0, r_base = 0, slot_q = -1;
     bool exhausted = false, have_tile = false;
     float t_thr_raw = INF;
-    unsigned q_mask = 0;  // queued slots (their first R*HS rows done)
-    int64_t q_base = 0;   // entry of slot 0
-    uint32_t q_cand = 0;  // candidate of this lane's queued slot
+    unsigned q_mask = 0;  // queued slots
+    uint32_t q_cand = 0;  // candidate and next row of this lane's queued slot
+    int q_i = 0;
     int head_h = -1;      // >= 0: a head batch is running, at head step head_h
     // reservoir: lane m holds entry r_base + m of the tile
     uint32_t pf_c = 0;
     float pf_lb = 0.f, pf_res = 0.f;
     // lane state
-    bool busy = false;
     int64_t ent = 0;
-    int i = 0, since = 0;
+    int i = -1;  // next row of the lane's pair; < 0: the lane is free
     uint32_t cand = 0;
     float c[RD], nc[RD];
     float thr = INF, thr_pend_raw = INF, lbtot = 0.f, prefix = 0.f;
     int cq = -1;
-    unsigned c_comp = 0, c_ab = 0, c_cells = 0, c_issued = 0;  // flushed before 2^31
+    // abandons are counted as computed minus the (rare) completions
+    unsigned c_comp = 0, c_cells = 0, c_issued = 0;  // flushed before 2^31
     auto flush = [&]() {
         if (cq >= 0) {
             unsigned long long* ctr = reinterpret_cast<unsigned long long*>(a.counters + (int64_t)cq * TCDTW_COUNTERS);
-            if (c_comp) atomicAdd(ctr + TCDTW_C_DTW_COMPUTED, (unsigned long long)c_comp);
-            if (c_ab) atomicAdd(ctr + TCDTW_C_ABANDON_COUNT, (unsigned long long)c_ab);
+            if (c_comp) {
+                atomicAdd(ctr + TCDTW_C_DTW_COMPUTED, (unsigned long long)c_comp);
+                atomicAdd(ctr + TCDTW_C_ABANDON_COUNT, (unsigned long long)c_comp);
+            }
             if (c_cells) atomicAdd(ctr + TCDTW_C_DTW_CELLS, (unsigned long long)c_cells);
             if (c_issued) atomicAdd(ctr + TCDTW_C_CELLS_ISSUED, (unsigned long long)c_issued);
         }
-        c_comp = c_ab = c_cells = c_issued = 0;
+        c_comp = c_cells = c_issued = 0;
     };
     auto load_rows = [&](float (&dst)[RD], uint32_t cc, int row) {  // rows row..row+R-1, row % R == 0
         const float4* src = reinterpret_cast<const float4*>(a.cands + ((int64_t)cc * n + row) * D);
@@ -1611,8 +1609,6 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
         for (int k = 0; k < B; ++k) ps[k * 32] = (k == W) ? 0.f : INF;
         load_rows(c, cc, 0);
         i = 0;
-        since = 0;
-        busy = true;
     };
     // next tile (warp-uniform); false when none is left
     auto next_tile = [&]() -> bool {
@@ -1635,7 +1631,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     // Body refill: free lanes take queued pairs; with the queue empty, either
     // a head batch starts (heads) or fresh pairs start at row 0 (no heads).
     auto refill = [&]() {
-        unsigned freem = __ballot_sync(FULL, !busy);
+        unsigned freem = __ballot_sync(FULL, i < 0);
         if (freem == 0) return;
         // queued pairs go to any free lane at once (a pop is a few loads); fresh
         // tile entries wait until refill_min lanes are free
@@ -1646,27 +1642,26 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                 const int rank = __popc(freem & ((1u << lane) - 1u));
                 const int sl = (int)__fns(q_mask, 0, (rank < take ? rank : 0) + 1);
                 const uint32_t cs = __shfl_sync(FULL, q_cand, sl);
-                if (!busy && rank < take) {
+                const int is = __shfl_sync(FULL, q_i, sl);
+                if (i < 0 && rank < take) {
                     if (slot_q != cq) {  // the lane's last pair may belong to the previous query
                         flush();
                         cq = slot_q;
                     }
-                    ent = q_base + sl;
                     cand = cs;
+                    load_rows(c, cand, is);
+                    ent = (int64_t)(uint32_t)q_el[sl] | ((int64_t)q_eh[sl] << 32);
                     lbtot = q_lb[sl];
-                    prefix = q_lb[32 + sl];
-                    i = R * HS;
-                    load_rows(c, cand, i);
+                    prefix = q_pre[sl];
 #pragma unroll
-                    for (int k = 0; k < B; ++k) ps[k * 32] = queue_band[k * 32 + sl];
+                    for (int k = 0; k < B; ++k) ps[k * 32] = q_band[k * 32 + sl];
                     const float raw = a.abandon ? load_volatile(a.thr_src + slot_q) : INF;
                     thr = a.abandon ? scale_up<float>(raw, a.mg) : INF;
                     thr_pend_raw = raw;
-                    since = 0;
-                    busy = true;
+                    i = is;
                 }
                 for (int k = 0; k < take; ++k) q_mask &= q_mask - 1;  // the lowest `take` slots are gone
-                freem = __ballot_sync(FULL, !busy);
+                freem = __ballot_sync(FULL, i < 0);
                 continue;
             }
             if (exhausted) return;
@@ -1680,24 +1675,27 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                 load_query(t_q);
             }
             if (heads) {
-                // head batch: park the busy lanes, take the next (up to) 32
+                // head batch: the busy lanes' pairs go to the queue (the queue
+                // is empty here), every lane takes one of the next (up to) 32
                 // entries of the tile -- the reservoir window, lane m <-> entry
-                // r_base + m (batches consume whole windows) -- one per lane
-                park_busy[lane] = busy ? 1 : 0;
-                if (busy) {
-                    park_i[lane] = i;
-                    park_el[lane] = (int)(uint32_t)ent;
-                    park_eh[lane] = (int)(ent >> 32);
-                    park_c[lane] = cand;
-                    park_lb[lane] = lbtot;
-                    park_pre[lane] = prefix;
+                // r_base + m (batches consume whole windows) -- and keeps it
+                // after the head steps; free lanes pop the queued pairs
+                q_mask = __ballot_sync(FULL, i >= 0);
+                if (i >= 0) {
+                    q_cand = cand;
+                    q_i = i;
+                    q_el[lane] = (int)(uint32_t)ent;
+                    q_eh[lane] = (int)(ent >> 32);
+                    q_lb[lane] = lbtot;
+                    q_pre[lane] = prefix;
 #pragma unroll
-                    for (int k = 0; k < B; ++k) park_band[k * 32] = ps[k * 32];
+                    for (int k = 0; k < B; ++k) q_band[k * 32 + lane] = ps[k * 32];
                 }
-                busy = false;
+                __syncwarp();
+                i = -1;
                 const int avail = min(t_len - t_next, 32);
-                q_base = t_begin + t_next;
-                if (lane < avail && !(pf_res < 0.f)) start_pair(q_base + lane, pf_c, pf_lb);
+                const int64_t e0 = t_begin + t_next;
+                if (lane < avail && !(pf_res < 0.f)) start_pair(e0 + lane, pf_c, pf_lb);
                 t_next += avail;
                 if (t_next < t_len) {
                     r_base += 32;
@@ -1718,43 +1716,11 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
             const uint32_t c_m = __shfl_sync(FULL, pf_c, m);
             const float lb_m = __shfl_sync(FULL, pf_lb, m);
             const float res_m = __shfl_sync(FULL, pf_res, m);
-            if (!busy && rank < take && !(res_m < 0.f))  // skip entries pruned by the advanced bound
+            if (i < 0 && rank < take && !(res_m < 0.f))  // skip entries pruned by the advanced bound
                 start_pair(t_begin + r_base + m, c_m, lb_m);
             t_next += take;
-            freem = __ballot_sync(FULL, !busy);
+            freem = __ballot_sync(FULL, i < 0);
         }
-    };
-    // The head batch is over: survivors join the queue (slot = their lane),
-    // parked lanes resume -- their next rows were prefetched into nc during
-    // the last head step.
-    auto end_heads = [&]() {
-        q_mask = __ballot_sync(FULL, busy);
-        if (busy) {
-            q_cand = cand;
-            q_lb[lane] = lbtot;
-            q_lb[32 + lane] = prefix;
-#pragma unroll
-            for (int k = 0; k < B; ++k) queue_band[k * 32 + lane] = ps[k * 32];
-        }
-        __syncwarp();
-        busy = park_busy[lane] != 0;
-        if (busy) {
-            i = park_i[lane];
-            ent = (int64_t)(uint32_t)park_el[lane] | ((int64_t)park_eh[lane] << 32);
-            cand = park_c[lane];
-            lbtot = park_lb[lane];
-            prefix = park_pre[lane];
-#pragma unroll
-            for (int k = 0; k < B; ++k) ps[k * 32] = park_band[k * 32];
-            const float raw = a.abandon ? load_volatile(a.thr_src + slot_q) : INF;
-            thr = a.abandon ? scale_up<float>(raw, a.mg) : INF;
-            thr_pend_raw = raw;
-#pragma unroll
-            for (int u = 0; u < RD; ++u) c[u] = nc[u];
-            since = 0;
-        }
-        __syncwarp();
-        head_h = -1;
     };
     float cur[R], prv[R], pu = 0.f, rmin = INF;
     // iteration s of the step: window column i - W + s for rows i..i+R-1.
@@ -1806,18 +1772,16 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     while (true) {
         if (head_h < 0) {
             refill();
-            if (!__any_sync(FULL, busy) && exhausted && q_mask == 0) break;
+            if (!__any_sync(FULL, i >= 0) && exhausted && q_mask == 0) break;
         }
         // head step h: rows i = R h .. with the first (W - i) / R blocks
         // skipped (their columns are < 0); body steps start at block 0
         const int j0 = head_h >= 0 ? (W - R * head_h) / R : 0;
         c_issued += head_h >= 0 ? R * (B - R * j0) + R * (R - 1) / 2 : R * B;
         if (c_cells >= (1u << 30) || c_issued >= (1u << 30)) flush();
-        const bool last_head = head_h == HS - 1;
-        if (last_head && park_busy[lane]) load_rows(nc, park_c[lane], park_i[lane]);  // the parked pair's rows
-        if (busy) {
+        if (i >= 0) {
             const bool more = i + R < n;
-            if (more && !last_head) load_rows(nc, cand, i + R);  // consumed after the DP
+            if (more) load_rows(nc, cand, i + R);  // consumed after the DP
 #pragma unroll
             for (int r = 0; r < R; ++r) cur[r] = prv[r] = INF;
             rmin = INF;
@@ -1877,24 +1841,24 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                 if (!abandoned) {
                     atomic_min_nonneg<float>(a.dbest + cq, fin);
                     note_done(a, cq, ent);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + (int64_t)cq * TCDTW_COUNTERS) +
+                                  TCDTW_C_ABANDON_COUNT,
+                              ~0ull);  // one completion: -1 (mod 2^64) against the flushed c_comp
                 }
                 ++c_comp;
-                c_ab += abandoned ? 1 : 0;
                 c_cells += cells_upto(stop, n, W);
-                busy = false;
+                i = -1;
             } else {
                 i += R;
 #pragma unroll
                 for (int u = 0; u < RD; ++u) c[u] = nc[u];
-                since += R;
-                if (since >= a.thr_every) {
-                    since = 0;
+                if ((i & thr_mask) == 0) {  // every thr_every rows (a power of two)
                     thr = scale_up<float>(thr_pend_raw, a.mg);
                     if (a.abandon) thr_pend_raw = load_volatile(a.thr_src + cq);
                 }
             }
         }
-        if (head_h >= 0 && ++head_h == HS) end_heads();
+        if (head_h >= 0 && ++head_h == HS) head_h = -1;  // the fresh pairs carry on in their lanes
     }
     flush();
 }
@@ -1918,6 +1882,9 @@ static int laner_rows(const SArgs<float>& a, int d, int B) {
     return laner_rows_shape(a.n, d, B);
 }
 
+#ifndef TCDTW_LANER_MINB
+#define TCDTW_LANER_MINB 8
+#endif
 static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n_tiles, const uint32_t* cand_of,
                         float* res, int* tctr, cudaStream_t st) {
     constexpr int threads = 64;
@@ -1947,7 +1914,7 @@ static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n
 #define TCDTW_LANER_CASE(DD, BB, RR)                                                          \
     if (d == DD && B == BB && a.n % RR == 0) {                                                \
         const int ww = LaneRLayout<DD, RR>::warp_words(a.n, a.qpad_rows, BB);                 \
-        return go(dtw_laner_kernel<DD, BB, RR, true, 8>, ww);                                 \
+        return go(dtw_laner_kernel<DD, BB, RR, true, TCDTW_LANER_MINB>, ww);                                 \
     }
     TCDTW_LANER_SPECS(TCDTW_LANER_CASE)
 #undef TCDTW_LANER_CASE
