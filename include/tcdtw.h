@@ -163,10 +163,11 @@ typedef struct tcdtw_search_desc {
      * default); when it overflows, every survivor tile is scanned instead.
      * Tests set 1 to exercise that path (ABI version 3). */
     int64_t done_cap;
-    /* Optional (ABI version 3): the candidates in the planar layout the
-     * LB_MV pass reads, (n * dims, n_candidates) of `dtype`, made once per
-     * collection with tcdtw_planarize; NULL = planarised into the workspace
-     * on every call.  Ignored with TCDTW_FLAG_F32_FILTER. */
+    /* Optional (ABI version 3; trailer since 4): the candidates in the
+     * planar layout the LB_MV pass reads, made once per collection with
+     * tcdtw_planarize into tcdtw_planar_bytes(...) bytes; NULL = planarised
+     * into the workspace on every call.  Ignored with TCDTW_FLAG_F32_FILTER
+     * and, for float32, with TCDTW_FLAG_REVERSE_LB. */
     const void *cand_planar;
     /* Candidate-side box sets (ABI version 3): every
      * candidate's LB_PC boxes, (n_candidates, G, max_boxes, dims) lo / hi of
@@ -250,7 +251,18 @@ int tcdtw_nn_search(const tcdtw_search_desc *desc, const void *queries, const vo
                     double *best_distance, int64_t *counters, void *stream);
 
 /* The planar copy of a collection for tcdtw_search_desc.cand_planar:
- * series (n_series, n, dims) -> out (n * dims, n_series), dtype elements. */
+ * series (n_series, n, dims) -> out (n * dims, n_series), dtype elements,
+ * followed by a trailer; `out` holds tcdtw_planar_bytes(...) bytes (ABI
+ * version 4).  The copy is opaque: float32 values are multiplied by a power
+ * of two sigma that maps the collection's value range into (1/2, 1] (exact),
+ * and the trailer keeps {sigma, 1/sigma}.  The LB_MV pass then evaluates a
+ * per-dimension envelope deviation as sat(|c - m| - h) on (midpoint, half
+ * width) query envelopes -- FADD, FADD.SAT, FFMA instead of the five
+ * operations of max(c - u, l - c, 0) (lb_mv.py:91-104) -- with h inflated so
+ * the float32 value never exceeds the real deviation by more than two
+ * roundings; a deviation above the collection's range saturates (a weaker,
+ * still valid bound).  Returns 0 on invalid arguments. */
+size_t tcdtw_planar_bytes(int dtype, int64_t n_series, int32_t n, int32_t dims);
 int tcdtw_planarize(int dtype, const void *series, int64_t n_series, int32_t n, int32_t dims, void *out,
                     void *stream);
 

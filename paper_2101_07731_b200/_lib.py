@@ -85,6 +85,7 @@ _SIGS = {
                              _vp], ctypes.c_int),
     "tcdtw_nn_search": ([ctypes.POINTER(SearchDesc), _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp],
                         ctypes.c_int),
+    "tcdtw_planar_bytes": ([ctypes.c_int, _i64, _i32, _i32], ctypes.c_size_t),
     "tcdtw_planarize": ([ctypes.c_int, _vp, _i64, _i32, _i32, _vp, _vp], ctypes.c_int),
     "tcdtw_shard_combine": ([_vp, _i32, _i64, _vp, _vp, _vp], ctypes.c_int),
     "tcdtw_lb_mv_matrix": ([ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp], ctypes.c_int),

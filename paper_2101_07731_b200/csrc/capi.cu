@@ -38,6 +38,7 @@ size_t normalize_workspace_bytes(int64_t, int);
 int normalize_f64(const double*, int64_t, int, double*, double*, double*, double*, double*, cudaStream_t);
 int shard_combine(const int64_t*, int, int64_t, int64_t*, double*, cudaStream_t);
 int planarize_series(int, const void*, int64_t, int, int, void*, cudaStream_t);
+size_t planar_copy_bytes(int, int64_t, int, int);
 }  // namespace tcdtw
 
 using namespace tcdtw;
@@ -62,7 +63,7 @@ const char* tcdtw_strerror(int status) {
     }
 }
 
-int tcdtw_abi_version(void) { return 3; }  // 3: tcdtw_parse_text, normalize workspace by size
+int tcdtw_abi_version(void) { return 4; }  // 4: planar copies carry a scale trailer (tcdtw_planar_bytes)
 
 unsigned long long tcdtw_launch_count(void) { return g_launches.load(); }
 
@@ -207,6 +208,10 @@ int tcdtw_normalize(const double* values, int64_t n_points, int32_t dims, double
     if (!values || !out || !mean || !std_ || !range) return TCDTW_INVALID_INPUT;
     if (!workspace || ws_bytes < normalize_workspace_bytes(n_points, dims)) return TCDTW_WORKSPACE_TOO_SMALL;
     return normalize_f64(values, n_points, dims, out, mean, std_, range, (double*)workspace, S(stream));
+}
+size_t tcdtw_planar_bytes(int dtype, int64_t n_series, int32_t n, int32_t dims) {
+    if (!dtype_ok(dtype) || n_series < 0 || n < 1 || dims < 1) return 0;
+    return planar_copy_bytes(dtype, n_series, n, dims);
 }
 int tcdtw_planarize(int dtype, const void* series, int64_t n_series, int32_t n, int32_t dims, void* out,
                     void* stream) {

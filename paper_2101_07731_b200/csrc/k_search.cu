@@ -80,9 +80,23 @@ const char* dtw_kernel_name(const tcdtw_search_desc* dsc) {
 }
 
 int planarize_series(int dtype, const void* series, int64_t ns, int n, int d, void* out, cudaStream_t st) {
-    if (dtype == TCDTW_F64) return planarize<double>((const double*)series, ns, n * d, (double*)out, st);
-    if (dtype == TCDTW_F32) return planarize<float>((const float*)series, ns, n * d, (float*)out, st);
+    // elements + trailer {sigma, 1/sigma} (planar_bytes): float32 copies are scaled
+    if (dtype == TCDTW_F64) {
+        float* scale = reinterpret_cast<float*>(reinterpret_cast<char*>(out) + planar_trailer_off(ns, n * d, 8));
+        planar_scale_kernel<<<1, 1, 0, st>>>(nullptr, scale);
+        return planarize<double>((const double*)series, ns, n * d, (double*)out, st);
+    }
+    if (dtype == TCDTW_F32) {
+        float* scale = reinterpret_cast<float*>(reinterpret_cast<char*>(out) + planar_trailer_off(ns, n * d, 4));
+        const int rc = planar_scale((const float*)series, ns * n * d, scale, st);
+        if (rc != TCDTW_OK) return rc;
+        return planarize<float>((const float*)series, ns, n * d, (float*)out, st, scale);
+    }
     return TCDTW_INVALID_INPUT;
+}
+
+size_t planar_copy_bytes(int dtype, int64_t ns, int n, int d) {
+    return planar_bytes(ns, n * d, dtype == TCDTW_F64 ? 8 : 4);
 }
 
 int alu_probe(int dtype, int blocks, int iters, void* sink, double* lane_ops, cudaStream_t st) {

@@ -102,17 +102,24 @@ __device__ __forceinline__ float fin_up(float v, const Margins& mg) {
 }
 
 // ------------------------------------------------------- planar transpose
-// [s][t][p] -> [t*d+p][s]: operands of the tiled LB_MV kernel.
+// [s][t][p] -> [t*d+p][s]: operands of the tiled LB_MV kernel.  With `scale`
+// (float32 filter path) the values are multiplied by scale[0], a power of
+// two (exact): the saturating LB_MV pass works in the scaled domain.
 template <typename T>
-__global__ void planar_kernel(const T* __restrict__ in, int64_t S, int rows, T* __restrict__ out) {
+__global__ void planar_kernel(const T* __restrict__ in, int64_t S, int rows, T* __restrict__ out,
+                              const float* __restrict__ scale) {
     __shared__ T tile[32][33];
     const int64_t s0 = (int64_t)blockIdx.x * 32;
     const int r0 = blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    T sc = T(1);
+    if constexpr (std::is_same<T, float>::value) {
+        if (scale) sc = __ldg(scale);
+    }
     for (int k = ty; k < 32; k += 8) {
         const int64_t s = s0 + k;
         const int r = r0 + tx;
-        tile[k][tx] = (s < S && r < rows) ? in[s * rows + r] : T(0);
+        tile[k][tx] = (s < S && r < rows) ? in[s * rows + r] * sc : T(0);
     }
     __syncthreads();
     for (int k = ty; k < 32; k += 8) {
@@ -123,11 +130,91 @@ __global__ void planar_kernel(const T* __restrict__ in, int64_t S, int rows, T* 
 }
 
 template <typename T>
-int planarize(const T* in, int64_t S, int rows, T* out, cudaStream_t st) {
+int planarize(const T* in, int64_t S, int rows, T* out, cudaStream_t st, const float* scale = nullptr) {
     dim3 grid((unsigned)((S + 31) / 32), (unsigned)((rows + 31) / 32));
     if (grid.y > 65535) return TCDTW_NOT_SUPPORTED;
-    planar_kernel<T><<<grid, 256, 0, st>>>(in, S, rows, out);
+    planar_kernel<T><<<grid, 256, 0, st>>>(in, S, rows, out, scale);
     return launch_status();
+}
+
+// A planar copy carries a 256-byte trailer behind its elements: float[2]
+// {sigma, 1/sigma}, the power-of-two scale its values were multiplied by
+// (1 for float64).  sigma maps the collection's value range into (1/2, 1],
+// so a per-dimension envelope deviation of any query inside that range is
+// <= 1 in the scaled domain and FADD.SAT clamps only what is negative.
+inline size_t planar_trailer_off(int64_t S, int rows, size_t es) { return ((size_t)S * rows * es + 255) & ~size_t(255); }
+inline size_t planar_bytes(int64_t S, int rows, size_t es) { return planar_trailer_off(S, rows, es) + 256; }
+
+__device__ __forceinline__ unsigned f32_ordered(float v) {  // monotone float -> unsigned
+    const unsigned u = __float_as_uint(v);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float f32_unordered(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+// mm[0] = ordered min (init 0xffffffff), mm[1] = ordered max (init 0)
+static __global__ void __launch_bounds__(256) value_range_kernel(const float* __restrict__ v, int64_t count,
+                                                                 unsigned* __restrict__ mm) {
+    unsigned lo = 0xffffffffu, hi = 0u;
+    for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < count; e += (int64_t)gridDim.x * 256) {
+        const unsigned k = f32_ordered(v[e]);
+        lo = k < lo ? k : lo;
+        hi = k > hi ? k : hi;
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mm, lo);
+        atomicMax(mm + 1, hi);
+    }
+}
+static __global__ void planar_scale_kernel(const unsigned* __restrict__ mm, float* __restrict__ scale) {
+    float sg = 1.f;
+    if (mm && mm[0] <= mm[1]) {
+        const double range = (double)f32_unordered(mm[1]) - (double)f32_unordered(mm[0]);
+        if (range > 0.0) {
+            int ex;
+            frexp(range, &ex);  // range = f * 2^ex, f in [1/2, 1)
+            if (ldexp(1.0, ex - 1) == range) --ex;  // an exact power of two maps to 1
+            ex = ex > 126 ? 126 : (ex < -126 ? -126 : ex);
+            sg = (float)ldexp(1.0, -ex);
+        }
+    }
+    scale[0] = sg;
+    scale[1] = 1.f / sg;  // exact
+}
+// float32 collection -> its scale (mm: 8 bytes of scratch next to `scale`)
+static int planar_scale(const float* v, int64_t count, float* scale, cudaStream_t st) {
+    unsigned* mm = reinterpret_cast<unsigned*>(scale + 2);
+    cudaMemsetAsync(mm, 0xff, 4, st);
+    cudaMemsetAsync(mm + 1, 0, 4, st);
+    int64_t blocks = (count + 255) / 256;
+    blocks = blocks > 148 * 16 ? 148 * 16 : (blocks < 1 ? 1 : blocks);
+    value_range_kernel<<<(unsigned)blocks, 256, 0, st>>>(v, count, mm);
+    planar_scale_kernel<<<1, 1, 0, st>>>(mm, scale);
+    return launch_status();
+}
+
+// The query envelopes of the saturating LB_MV pass: planar (upper, lower) ->
+// (m, h) in the scaled domain, in place.  m = the rounded midpoint, h = the
+// half width inflated so that max(|c - m| - h, 0), evaluated in float32, is
+// <= dist(c, [lower, upper]) (1 + 2^-24)^2 for EVERY float c:
+//   h >= (true half width + |m - true midpoint|) (1 + 2^-22) + 2^-120
+// covers the rounding of m, of c - m and of |.| - h (the relative part) and
+// flushed subnormals of the scaled operands (the absolute part).
+static __global__ void __launch_bounds__(256) midhalf_kernel(float* __restrict__ up, float* __restrict__ lo,
+                                                             int64_t count, const float* __restrict__ scale) {
+    const float sg = __ldg(scale);
+    for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < count; e += (int64_t)gridDim.x * 256) {
+        const double u = (double)(up[e] * sg), l = (double)(lo[e] * sg);
+        const double md = 0.5 * (u + l);
+        const float m = (float)md;
+        const double em = fabs((double)m - md);
+        const double hd = (0.5 * (u - l) + em) * (1.0 + 0x1p-22) + 0x1p-120;
+        float h = __double2float_ru(hd * (1.0 + 0x1p-50));
+        up[e] = m;
+        lo[e] = h;
+    }
 }
 
 // ------------------------------------------------------------ LB_MV matrix
@@ -148,12 +235,13 @@ struct MvTile {
     static constexpr int CT = 16 * M;
 };
 
-template <typename T, int DMAX, bool EXACT, bool UB, int DX>
+template <typename T, int DMAX, bool EXACT, bool UB, int DX, bool SAT>
 __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT, const T* __restrict__ LT,
                                                         const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                         int64_t Q, int64_t N, int n, int d, int TC,
                                                         T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
-                                                        int64_t c0, bool v16, bool trans, int64_t ub_n, int ub_stride);
+                                                        int64_t c0, bool v16, bool trans, int64_t ub_n, int ub_stride,
+                                                        const float* __restrict__ scale);
 
 // asynchronous global -> shared copies; src_bytes < bytes zero-fills the rest
 __device__ __forceinline__ void cp_async_ca(void* dst, const void* src, int bytes, int src_bytes) {
@@ -173,12 +261,13 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // DX > 0: the dimension count is a compile-time constant (fully unrolled
 // per-dimension loop for the hot shapes); DX == 0: runtime d.
-template <typename T, int DMAX, bool EXACT, bool UB, int DX>
+template <typename T, int DMAX, bool EXACT, bool UB, int DX, bool SAT>
 __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ UT, const T* __restrict__ LT,
                                                           const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                           int64_t Q, int64_t N, int n, int d, int TC,
                                                           T* __restrict__ out, T* __restrict__ ub_out, int ub_stride,
-                                                          bool v16, bool trans, int64_t ub_n) {
+                                                          bool v16, bool trans, int64_t ub_n,
+                                                          const float* __restrict__ scale) {
     using Tile = MvTile<T, DMAX, EXACT>;
     constexpr int QT = Tile::QT, CTL = Tile::CT;
     // query tiles vary fastest: concurrently resident blocks share one
@@ -191,21 +280,22 @@ __global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ 
     // candidate tile (block-uniform)
     if constexpr (UB) {
         if (((int64_t)blockIdx.x / nqt) % ub_stride != 0) {
-            lbmv_matrix_kernel_body<T, DMAX, EXACT, false, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0,
-                                                               v16, trans, ub_n, ub_stride);
+            lbmv_matrix_kernel_body<T, DMAX, EXACT, false, DX, SAT>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0,
+                                                                    c0, v16, trans, ub_n, ub_stride, scale);
             return;
         }
     }
-    lbmv_matrix_kernel_body<T, DMAX, EXACT, UB, DX>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0, v16,
-                                                    trans, ub_n, ub_stride);
+    lbmv_matrix_kernel_body<T, DMAX, EXACT, UB, DX, SAT>(UT, LT, QTP, CT_, Q, N, n, d, TC, out, ub_out, q0, c0, v16,
+                                                         trans, ub_n, ub_stride, scale);
 }
 
-template <typename T, int DMAX, bool EXACT, bool UB, int DX>
+template <typename T, int DMAX, bool EXACT, bool UB, int DX, bool SAT>
 __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT, const T* __restrict__ LT,
                                                         const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                         int64_t Q, int64_t N, int n, int d, int TC,
                                                         T* __restrict__ out, T* __restrict__ ub_out, int64_t q0,
-                                                        int64_t c0, bool v16, bool trans, int64_t ub_n, int ub_stride) {
+                                                        int64_t c0, bool v16, bool trans, int64_t ub_n, int ub_stride,
+                                                        const float* __restrict__ scale) {
     using Tile = MvTile<T, DMAX, EXACT>;
     constexpr int M = Tile::M, QT = Tile::QT, CTL = Tile::CT;
     constexpr int VN = 16 / (int)sizeof(T);  // elements per 16-byte copy
@@ -357,8 +447,15 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
                     for (int i = 0; i < M; ++i)
 #pragma unroll
                         for (int j = 0; j < M; ++j) {
-                            // u >= l, so at most one of (c-u, l-c) is positive
-                            const T dev = tmax(tmax(c[j] - u[i], l[i] - c[j]), T(0));
+                            T dev;
+                            if constexpr (SAT) {
+                                // u = midpoint, l = inflated half width (midhalf_kernel), scaled
+                                // domain: FADD, FADD.SAT with |.|, FFMA -- 3 issue slots per term
+                                dev = __saturatef(fabsf(c[j] - u[i]) - l[i]);
+                            } else {
+                                // u >= l, so at most one of (c-u, l-c) is positive
+                                dev = tmax(tmax(c[j] - u[i], l[i] - c[j]), T(0));
+                            }
                             s[i][j] = fma(dev, dev, s[i][j]);
                             if constexpr (UB) {
                                 const T df = qv[i] - c[j];
@@ -376,6 +473,16 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
             }
         }
         __syncthreads();
+    }
+    if constexpr (SAT) {  // back from the scaled domain (a power of two: exact)
+        const T inv = (T)__ldg(scale + 1);
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                total[i][j] *= inv;
+                if constexpr (UB) ubt[i][j] *= inv;
+            }
     }
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -398,7 +505,8 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
 
 template <typename T, int DMAX, bool EXACT>
 int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int64_t Q, int64_t N, int n, int d,
-                       T* out, T* ub_out, cudaStream_t st, int ub_stride = 1, bool trans = false, int64_t ub_n = 0) {
+                       T* out, T* ub_out, cudaStream_t st, int ub_stride = 1, bool trans = false, int64_t ub_n = 0,
+                       const float* scale = nullptr) {
     using Tile = MvTile<T, DMAX, EXACT>;
     const bool ub = ub_out != nullptr;
     // two staging buffers of TC time steps each (layout us | ls | cs | qs)
@@ -411,12 +519,26 @@ int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int6
     const bool v16 = Q % VN == 0 && N % VN == 0 && (reinterpret_cast<uintptr_t>(UT) | reinterpret_cast<uintptr_t>(LT) |
                                                      reinterpret_cast<uintptr_t>(QTP) | reinterpret_cast<uintptr_t>(CT)) % 16 == 0 &&
                      (Tile::QT % VN) == 0 && (Tile::CT % VN) == 0;
-    auto kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true, 0> : lbmv_matrix_kernel<T, DMAX, EXACT, false, 0>;
+    // scale != nullptr: the saturating form (operands prepared by midhalf_kernel / scaled planarize)
+    constexpr bool CAN_SAT = !EXACT && std::is_same<T, float>::value;
+    const bool sat = CAN_SAT && scale != nullptr;
+    if (scale != nullptr && !sat) return TCDTW_NOT_SUPPORTED;
+    auto kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true, 0, false> : lbmv_matrix_kernel<T, DMAX, EXACT, false, 0, false>;
+    if constexpr (CAN_SAT) {
+        if (sat) kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true, 0, true> : lbmv_matrix_kernel<T, DMAX, EXACT, false, 0, true>;
+    }
     if constexpr (!EXACT) {
 #define TCDTW_MV_DX(DD)                                                                                    \
-        if (d == DD && DD <= DMAX)                                                                         \
-            kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true, (DD <= DMAX ? DD : 0)>                      \
-                      : lbmv_matrix_kernel<T, DMAX, EXACT, false, (DD <= DMAX ? DD : 0)>;
+        if (d == DD && DD <= DMAX) {                                                                       \
+            constexpr int DXV = DD <= DMAX ? DD : 0;                                                       \
+            kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true, DXV, false>                               \
+                      : lbmv_matrix_kernel<T, DMAX, EXACT, false, DXV, false>;                             \
+            if constexpr (CAN_SAT) {                                                                       \
+                if (sat)                                                                                   \
+                    kern = ub ? lbmv_matrix_kernel<T, DMAX, EXACT, true, DXV, true>                        \
+                              : lbmv_matrix_kernel<T, DMAX, EXACT, false, DXV, true>;                      \
+            }                                                                                              \
+        }
         TCDTW_MV_DX(3) TCDTW_MV_DX(4) TCDTW_MV_DX(5) TCDTW_MV_DX(6) TCDTW_MV_DX(8) TCDTW_MV_DX(20)
 #undef TCDTW_MV_DX
     }
@@ -428,7 +550,7 @@ int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int6
     const int64_t nct = (N + Tile::CT - 1) / Tile::CT;
     if (nqt * nct > 2147483647LL) return TCDTW_NOT_SUPPORTED;
     const unsigned grid = (unsigned)(nqt * nct);
-    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out, ub_stride, v16, trans, ub_n);
+    kern<<<grid, 256, smem, st>>>(UT, LT, QTP, CT, Q, N, n, d, TC, out, ub_out, ub_stride, v16, trans, ub_n, scale);
     return launch_status();
 }
 
@@ -3138,6 +3260,7 @@ struct Plan {
     bool has_lb, exact, rev;
     bool f32f;  // TCDTW_FLAG_F32_FILTER: float64 inputs, float32 filter
     bool cand_planar;  // desc->cand_planar is used instead of o_candT
+    bool sat;          // the saturating LB_MV pass on scaled planar operands (float32, no reverse bound)
     bool rev_pc;       // TCDTW_FLAG_REVERSE_PC with an LB_PC second stage
     size_t o_q32, o_c32, o_slack, o_lanesc, o_dbf;
     int64_t max_tiles;
@@ -3215,8 +3338,10 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     p.o_upT = take(p.has_lb ? series_q : 0);
     p.o_loT = take(p.has_lb ? series_q : 0);
     p.o_qT = take(p.has_lb ? series_q : 0);
-    p.cand_planar = p.has_lb && dsc->cand_planar != nullptr && !p.f32f;  // the caller keeps a planar copy
-    p.o_candT = take(p.has_lb && !p.cand_planar ? (size_t)N * p.n * p.d * es : 0);
+    p.sat = p.has_lb && !p.exact && !p.rev;
+    // the caller keeps a planar copy (a float32 one is scaled: not for the reverse bound's unscaled pass)
+    p.cand_planar = p.has_lb && dsc->cand_planar != nullptr && !p.f32f && (p.exact || p.sat);
+    p.o_candT = take(p.has_lb && !p.cand_planar ? planar_bytes(N, p.n * p.d, es) : 0);
     p.o_steps = take((size_t)Q * (p.n > 1 ? p.n - 1 : 1) * es);
     const size_t boxes = (size_t)Q * p.G * p.K * p.d * es;
     p.o_blo = take(boxes);
@@ -3374,7 +3499,8 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
         a.casc_hi = (T)(1.0 + s);
         a.casc_thr = (T)(1.0 + s);
     } else {
-        const double eps = (2.0 * p.n + p.d + 16.0) * 1.1920928955078125e-07;  // * 2^-23
+        // + 4: the saturating LB_MV terms carry two more roundings each (midhalf_kernel)
+        const double eps = (2.0 * p.n + p.d + 20.0) * 1.1920928955078125e-07;  // * 2^-23
         a.mg.prune = nextafterf((float)(1.0 + 3.0 * eps), 2.0f);
         a.mg.fin = nextafterf((float)(1.0 + 2.5 * eps), 2.0f);
         a.casc_lo = (T)(1.0 - eps);
@@ -3566,12 +3692,31 @@ struct SearchImpl {
         fill_kernel<T><<<grid_for(p.Q, 256), 256, 0, st>>>(a.dbest, p.Q, dev_inf<T>());
         TRY(launch_status());
         const T* candT = p.cand_planar ? (const T*)dsc->cand_planar : at<T>(ws, p.o_candT);
+        // {sigma, 1/sigma} of the planar candidates (their trailer)
+        const float* scale = nullptr;
+        if constexpr (!EXACT) {
+            if (p.sat)
+                scale = reinterpret_cast<const float*>(reinterpret_cast<const char*>(candT) +
+                                                       planar_trailer_off(p.N, p.n * p.d, p.es));
+        }
         if (p.has_lb) {
+            if constexpr (!EXACT) {
+                if (p.sat && !p.cand_planar)
+                    TRY(planar_scale((const float*)cands, p.N * p.n * p.d, const_cast<float*>(scale), st));
+            }
             TRY(series_envelope(dtype, queries, p.Q, p.n, p.d, p.w, at<T>(ws, p.o_up), at<T>(ws, p.o_lo), st));
             TRY(planarize<T>(at<T>(ws, p.o_up), p.Q, p.n * p.d, at<T>(ws, p.o_upT), st));
             TRY(planarize<T>(at<T>(ws, p.o_lo), p.Q, p.n * p.d, at<T>(ws, p.o_loT), st));
-            TRY(planarize<T>((const T*)queries, p.Q, p.n * p.d, at<T>(ws, p.o_qT), st));
-            if (!p.cand_planar) TRY(planarize<T>((const T*)cands, p.N, p.n * p.d, at<T>(ws, p.o_candT), st));
+            TRY(planarize<T>((const T*)queries, p.Q, p.n * p.d, at<T>(ws, p.o_qT), st, scale));
+            if (!p.cand_planar) TRY(planarize<T>((const T*)cands, p.N, p.n * p.d, at<T>(ws, p.o_candT), st, scale));
+            if constexpr (!EXACT) {
+                if (p.sat) {
+                    const int64_t cnt = p.Q * p.n * p.d;
+                    midhalf_kernel<<<grid_for(cnt, 256), 256, 0, st>>>(at<float>(ws, p.o_upT), at<float>(ws, p.o_loT),
+                                                                        cnt, scale);
+                    TRY(launch_status());
+                }
+            }
         }
         if (!EXACT) {
             const int DPq = (p.d + 1) / 2;
@@ -3591,7 +3736,7 @@ struct SearchImpl {
         if (p.has_lb)
             TRY((launch_lbmv_matrix<T, DMAX, EXACT>(at<T>(ws, p.o_upT), at<T>(ws, p.o_loT), at<T>(ws, p.o_qT),
                                                     candT, p.Q, p.N, p.n, p.d, at<T>(ws, p.o_lb),
-                                                    at<T>(ws, p.o_ub), st, p.ub_stride, false, p.ub_sampled)));
+                                                    at<T>(ws, p.o_ub), st, p.ub_stride, false, p.ub_sampled, scale)));
         if (p.rev) {
             // reverse LB_MV: the candidates' envelopes against the queries,
             // written transposed into the (query, candidate) layout

@@ -206,7 +206,8 @@ class SearchIndex:
             return None
         if self._planar is None:
             N, n, d = self.candidates.shape
-            planar = _dev.torch().empty((n * d, N), dtype=self.tdtype, device=self.candidates.device)
+            nbytes = _lib.lib().tcdtw_planar_bytes(_lib.dtype_code(self.dtype), N, n, d)  # elements + scale trailer
+            planar = _dev.torch().empty(nbytes, dtype=_dev.torch().uint8, device=self.candidates.device)
             _lib.check(_lib.lib().tcdtw_planarize(_lib.dtype_code(self.dtype), self.candidates.data_ptr(), N, n, d,
                                                   planar.data_ptr(), _lib.stream_ptr()), "planarize")
             self._planar = planar

@@ -294,6 +294,54 @@ def test_edge_cases(P, rng):
     check(const[0].astype(np.float32), const.astype(np.float32), 2, dtype="f32")
 
 
+
+@pytest.mark.parametrize("case", ["offset", "outside", "tiny", "huge", "ulps", "mixed_scale"])
+def test_saturating_lb_mv_adversarial(P, rng, case):
+    """float32 searches prune on the saturating LB_MV pass (scaled planar
+    operands, midpoint / inflated half-width envelopes, FADD.SAT): inputs
+    built to break a bound that is not a true lower bound -- a large common
+    offset (cancellation in c - m), queries far outside the collection's
+    range (saturation), tiny and huge magnitudes (power-of-two scales far
+    from 1), candidates within a few ulps of the query and of its
+    envelope, dimensions of very different scales -- still return the
+    oracle's index and distance."""
+    from oracle import oracle as O
+
+    n, d, w, N = 64, 6, 6, 700
+    walk = np.cumsum(rng.normal(size=(N, n, d)), axis=1)
+    queries = walk[:8] + 0.05 * rng.normal(size=(8, n, d))
+    if case == "offset":
+        cands, queries = 4096.0 + 1e-2 * walk, 4096.0 + 1e-2 * queries
+    elif case == "outside":
+        cands, queries = walk, queries * 3.0 + 500.0
+    elif case == "tiny":
+        cands, queries = walk * 1e-15, queries * 1e-15
+    elif case == "huge":
+        cands, queries = walk * 1e15, queries * 1e15
+    elif case == "ulps":
+        cands = walk.astype(np.float32)
+        queries = cands[:8].copy()
+        for k in range(8):  # candidates 100+k..: the query moved by a few ulps, up and down
+            for j in range(6):
+                steps = rng.integers(-2, 3, size=(n, d))
+                moved = cands[k].copy()
+                for _ in range(2):
+                    moved = np.where(steps > 0, np.nextafter(moved, np.float32(np.inf)),
+                                     np.where(steps < 0, np.nextafter(moved, np.float32(-np.inf)), moved))
+                cands[100 + 8 * j + k] = moved
+        cands[300:308] = cands[:8]  # exact duplicates: the lower index wins
+    else:  # mixed_scale
+        sc = np.array([1e-3, 1.0, 1e3, 1e-6, 30.0, 1e5])
+        cands, queries = walk * sc, queries * sc
+    cands = np.ascontiguousarray(cands, dtype=np.float32)
+    queries = np.ascontiguousarray(queries, dtype=np.float32)
+    res = P.SearchIndex(cands, dtype="f32").search(queries, _params(P, w, "lb_mv"))
+    outs, _ = O.nn_search_batch(queries.astype(np.float64), cands.astype(np.float64), O.make_params(w, "lb_mv"),
+                                None, None)
+    assert np.array_equal(res.best_index, np.array([o.best_index for o in outs]))
+    assert np.array_equal(res.best_distance, np.array([o.best_distance for o in outs]))
+
+
 def test_errors(P, rng):
     with pytest.raises(P.InvalidInputError):
         P.nn_search(rng.normal(size=(5, 2)), [], P.SearchParams(window=2))

@@ -20,7 +20,7 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(L, name), name
     assert set(_lib.EXPORTED) == declared
-    assert L.tcdtw_abi_version() == 3
+    assert L.tcdtw_abi_version() == 4
     assert L.tcdtw_strerror(1) == b"invalid input"
 
 
