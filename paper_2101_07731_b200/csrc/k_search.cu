@@ -90,7 +90,7 @@ int planarize_series(int dtype, const void* series, int64_t ns, int n, int d, vo
         float* scale = reinterpret_cast<float*>(reinterpret_cast<char*>(out) + planar_trailer_off(ns, n * d, 4));
         const int rc = planar_scale((const float*)series, ns * n * d, scale, st);
         if (rc != TCDTW_OK) return rc;
-        return planarize<float>((const float*)series, ns, n * d, (float*)out, st, scale);
+        return planarize_tiled((const float*)series, ns, n * d, (float*)out, st, scale);
     }
     return TCDTW_INVALID_INPUT;
 }

@@ -102,24 +102,17 @@ __device__ __forceinline__ float fin_up(float v, const Margins& mg) {
 }
 
 // ------------------------------------------------------- planar transpose
-// [s][t][p] -> [t*d+p][s]: operands of the tiled LB_MV kernel.  With `scale`
-// (float32 filter path) the values are multiplied by scale[0], a power of
-// two (exact): the saturating LB_MV pass works in the scaled domain.
+// [s][t][p] -> [t*d+p][s]: operands of the tiled LB_MV kernel.
 template <typename T>
-__global__ void planar_kernel(const T* __restrict__ in, int64_t S, int rows, T* __restrict__ out,
-                              const float* __restrict__ scale) {
+__global__ void planar_kernel(const T* __restrict__ in, int64_t S, int rows, T* __restrict__ out) {
     __shared__ T tile[32][33];
     const int64_t s0 = (int64_t)blockIdx.x * 32;
     const int r0 = blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    T sc = T(1);
-    if constexpr (std::is_same<T, float>::value) {
-        if (scale) sc = __ldg(scale);
-    }
     for (int k = ty; k < 32; k += 8) {
         const int64_t s = s0 + k;
         const int r = r0 + tx;
-        tile[k][tx] = (s < S && r < rows) ? in[s * rows + r] * sc : T(0);
+        tile[k][tx] = (s < S && r < rows) ? in[s * rows + r] : T(0);
     }
     __syncthreads();
     for (int k = ty; k < 32; k += 8) {
@@ -130,10 +123,42 @@ __global__ void planar_kernel(const T* __restrict__ in, int64_t S, int rows, T* 
 }
 
 template <typename T>
-int planarize(const T* in, int64_t S, int rows, T* out, cudaStream_t st, const float* scale = nullptr) {
+int planarize(const T* in, int64_t S, int rows, T* out, cudaStream_t st) {
     dim3 grid((unsigned)((S + 31) / 32), (unsigned)((rows + 31) / 32));
     if (grid.y > 65535) return TCDTW_NOT_SUPPORTED;
-    planar_kernel<T><<<grid, 256, 0, st>>>(in, S, rows, out, scale);
+    planar_kernel<T><<<grid, 256, 0, st>>>(in, S, rows, out);
+    return launch_status();
+}
+
+// The float32 planar copies of the saturating LB_MV pass are tile-major:
+// element (row r, series s) at ((s / 64) * rows + r) * 64 + s % 64, the last
+// tile zero-padded -- a tile's rows are contiguous (one TMA bulk copy per
+// operand and round) -- and multiplied by scale[0], a power of two (exact).
+constexpr int kPlanarTile = 64;
+inline int64_t planar_pad(int64_t S) { return (S + kPlanarTile - 1) / kPlanarTile * kPlanarTile; }
+static __global__ void planar_tiled_kernel(const float* __restrict__ in, int64_t S, int rows, float* __restrict__ out,
+                                           const float* __restrict__ scale) {
+    __shared__ float tile[32][33];
+    const int64_t s0 = (int64_t)blockIdx.x * 32;
+    const int r0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const float sc = __ldg(scale);
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t s = s0 + k;
+        const int r = r0 + tx;
+        tile[k][tx] = (s < S && r < rows) ? in[s * rows + r] * sc : 0.f;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        const int r = r0 + k;
+        const int64_t s = s0 + tx;  // < planar_pad(S): the grid covers whole tiles
+        if (r < rows) out[((s / kPlanarTile) * rows + r) * kPlanarTile + (s % kPlanarTile)] = tile[tx][k];
+    }
+}
+static int planarize_tiled(const float* in, int64_t S, int rows, float* out, cudaStream_t st, const float* scale) {
+    dim3 grid((unsigned)(planar_pad(S) / 32), (unsigned)((rows + 31) / 32));
+    if (grid.y > 65535) return TCDTW_NOT_SUPPORTED;
+    planar_tiled_kernel<<<grid, 256, 0, st>>>(in, S, rows, out, scale);
     return launch_status();
 }
 
@@ -142,7 +167,10 @@ int planarize(const T* in, int64_t S, int rows, T* out, cudaStream_t st, const f
 // (1 for float64).  sigma maps the collection's value range into (1/2, 1],
 // so a per-dimension envelope deviation of any query inside that range is
 // <= 1 in the scaled domain and FADD.SAT clamps only what is negative.
-inline size_t planar_trailer_off(int64_t S, int rows, size_t es) { return ((size_t)S * rows * es + 255) & ~size_t(255); }
+inline size_t planar_trailer_off(int64_t S, int rows, size_t es) {
+    const int64_t cols = es == 4 ? planar_pad(S) : S;  // float32 copies are tile-major, padded
+    return ((size_t)cols * rows * es + 255) & ~size_t(255);
+}
 inline size_t planar_bytes(int64_t S, int rows, size_t es) { return planar_trailer_off(S, rows, es) + 256; }
 
 __device__ __forceinline__ unsigned f32_ordered(float v) {  // monotone float -> unsigned
@@ -196,17 +224,16 @@ static int planar_scale(const float* v, int64_t count, float* scale, cudaStream_
 }
 
 // The query envelopes of the saturating LB_MV pass: planar (upper, lower) ->
-// (m, h) in the scaled domain, in place.  m = the rounded midpoint, h = the
+// (m, h), in place (scaled, tile-major; the layout does not matter here).  m = the rounded midpoint, h = the
 // half width inflated so that max(|c - m| - h, 0), evaluated in float32, is
 // <= dist(c, [lower, upper]) (1 + 2^-24)^2 for EVERY float c:
 //   h >= (true half width + |m - true midpoint|) (1 + 2^-22) + 2^-120
 // covers the rounding of m, of c - m and of |.| - h (the relative part) and
 // flushed subnormals of the scaled operands (the absolute part).
 static __global__ void __launch_bounds__(256) midhalf_kernel(float* __restrict__ up, float* __restrict__ lo,
-                                                             int64_t count, const float* __restrict__ scale) {
-    const float sg = __ldg(scale);
+                                                             int64_t count) {
     for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < count; e += (int64_t)gridDim.x * 256) {
-        const double u = (double)(up[e] * sg), l = (double)(lo[e] * sg);
+        const double u = (double)up[e], l = (double)lo[e];  // already scaled (planarize_tiled)
         const double md = 0.5 * (u + l);
         const float m = (float)md;
         const double em = fabs((double)m - md);
@@ -258,6 +285,27 @@ __device__ __forceinline__ void cp_async_cg16(void* dst, const void* src, int sr
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int NPEND>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NPEND) : "memory"); }
+// TMA bulk copies (global -> shared, bytes a multiple of 16) completing on an mbarrier
+__device__ __forceinline__ unsigned mv_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mv_bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     mv_saddr(dst)),
+                 "l"(src), "r"(bytes), "r"(mv_saddr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mv_bar_expect(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mv_saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mv_bar_wait(uint64_t* bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(mv_saddr(bar)), "r"(parity)
+            : "memory");
+    }
+}
 
 // DX > 0: the dimension count is a compile-time constant (fully unrolled
 // per-dimension loop for the hot shapes); DX == 0: runtime d.
@@ -300,10 +348,16 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
     constexpr int M = Tile::M, QT = Tile::QT, CTL = Tile::CT;
     constexpr int VN = 16 / (int)sizeof(T);  // elements per 16-byte copy
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    // two staging buffers (cp.async double buffering): round k+1's rows
+    // two staging buffers (double buffering): round k+1's rows
     // stream in while round k is consumed.  Buffer layout: us | ls | cs | qs
     const size_t buf_elems = (size_t)TC * d * (3 * QT + CTL);
     const int tid = threadIdx.x;
+    // SAT: the operands are tile-major planar copies (planar_tiled_kernel) --
+    // the rows of one 64-series tile are contiguous, so a round of every
+    // operand is ONE TMA bulk copy issued by thread 0, completing on the
+    // buffer's mbarrier; no staging instructions in the compute warps.
+    uint64_t* const bars = reinterpret_cast<uint64_t*>(reinterpret_cast<T*>(smem_raw) + 2 * buf_elems);
+    constexpr bool tma = SAT;
     auto stage = [&](int t0, int buf) {
         T* us = reinterpret_cast<T*>(smem_raw) + buf * buf_elems;
         T* ls = us + (size_t)TC * d * QT;
@@ -312,6 +366,19 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
         const int tcn = (n - t0) < TC ? (n - t0) : TC;
         const int rows = tcn * d;
         const int64_t rbase = (int64_t)t0 * d;
+        if constexpr (tma) {
+            static_assert(!SAT || (QT == kPlanarTile && CTL == kPlanarTile), "tile-major planar width");
+            if (tid != 0) return;
+            const unsigned bytes = (unsigned)rows * QT * (unsigned)sizeof(T);
+            const int64_t qoff = ((q0 / QT) * (int64_t)n * d + rbase) * QT;
+            const int64_t coff = ((c0 / CTL) * (int64_t)n * d + rbase) * CTL;
+            mv_bar_expect(bars + buf, (UB ? 4u : 3u) * bytes);
+            mv_bulk_load(us, UT + qoff, bytes, bars + buf);
+            mv_bulk_load(ls, LT + qoff, bytes, bars + buf);
+            if constexpr (UB) mv_bulk_load(qs, QTP + qoff, bytes, bars + buf);
+            mv_bulk_load(cs, CT_ + coff, bytes, bars + buf);
+            return;
+        }
         if (v16) {
             for (int e = tid * VN; e < rows * QT; e += 256 * VN) {
                 const int r = e / QT, qq = e - (e / QT) * QT;
@@ -356,17 +423,30 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
 #pragma unroll
         for (int j = 0; j < M; ++j) total[i][j] = ubt[i][j] = T(0);
 
-    stage(0, 0);
-    int buf = 0;
-    for (int t0 = 0; t0 < n; t0 += TC, buf ^= 1) {
-        const int tcn = (n - t0) < TC ? (n - t0) : TC;
-        if (t0 + TC < n) {
-            stage(t0 + TC, buf ^ 1);  // the other buffer was released by the barrier closing the last round
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
+    if constexpr (tma) {
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mv_saddr(bars)) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mv_saddr(bars + 1)) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
+    }
+    stage(0, 0);
+    int buf = 0, round = 0;
+    for (int t0 = 0; t0 < n; t0 += TC, buf ^= 1, ++round) {
+        const int tcn = (n - t0) < TC ? (n - t0) : TC;
+        if constexpr (tma) {
+            if (t0 + TC < n) stage(t0 + TC, buf ^ 1);  // the other buffer was released by the barrier closing the last round
+            mv_bar_wait(bars + buf, (unsigned)(round >> 1) & 1u);
+        } else {
+            if (t0 + TC < n) {
+                stage(t0 + TC, buf ^ 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+        }
         const T* us = reinterpret_cast<const T*>(smem_raw) + buf * buf_elems;
         const T* ls = us + (size_t)TC * d * QT;
         const T* cs = ls + (size_t)TC * d * QT;
@@ -514,7 +594,7 @@ int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int6
     int TC = (int)((96 * 1024) / (2 * per_t));
     TC = TC < 1 ? 1 : (TC > 16 ? 16 : TC);
     TC = TC > n ? n : TC;
-    const size_t smem = 2 * per_t * TC;
+    const size_t smem = 2 * per_t * TC + 16;  // + the two mbarriers of the TMA staging
     constexpr int VN = 16 / (int)sizeof(T);
     const bool v16 = Q % VN == 0 && N % VN == 0 && (reinterpret_cast<uintptr_t>(UT) | reinterpret_cast<uintptr_t>(LT) |
                                                      reinterpret_cast<uintptr_t>(QTP) | reinterpret_cast<uintptr_t>(CT)) % 16 == 0 &&
@@ -3335,9 +3415,10 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     const size_t series_q = (size_t)Q * p.n * p.d * es;
     p.o_up = take(p.has_lb ? series_q : 0);
     p.o_lo = take(p.has_lb ? series_q : 0);
-    p.o_upT = take(p.has_lb ? series_q : 0);
-    p.o_loT = take(p.has_lb ? series_q : 0);
-    p.o_qT = take(p.has_lb ? series_q : 0);
+    const size_t planar_q = (size_t)(es == 4 ? planar_pad(Q) : Q) * p.n * p.d * es;  // float32: whole tiles
+    p.o_upT = take(p.has_lb ? planar_q : 0);
+    p.o_loT = take(p.has_lb ? planar_q : 0);
+    p.o_qT = take(p.has_lb ? planar_q : 0);
     p.sat = p.has_lb && !p.exact && !p.rev;
     // the caller keeps a planar copy (a float32 one is scaled: not for the reverse bound's unscaled pass)
     p.cand_planar = p.has_lb && dsc->cand_planar != nullptr && !p.f32f && (p.exact || p.sat);
@@ -3705,17 +3786,27 @@ struct SearchImpl {
                     TRY(planar_scale((const float*)cands, p.N * p.n * p.d, const_cast<float*>(scale), st));
             }
             TRY(series_envelope(dtype, queries, p.Q, p.n, p.d, p.w, at<T>(ws, p.o_up), at<T>(ws, p.o_lo), st));
-            TRY(planarize<T>(at<T>(ws, p.o_up), p.Q, p.n * p.d, at<T>(ws, p.o_upT), st));
-            TRY(planarize<T>(at<T>(ws, p.o_lo), p.Q, p.n * p.d, at<T>(ws, p.o_loT), st));
-            TRY(planarize<T>((const T*)queries, p.Q, p.n * p.d, at<T>(ws, p.o_qT), st, scale));
-            if (!p.cand_planar) TRY(planarize<T>((const T*)cands, p.N, p.n * p.d, at<T>(ws, p.o_candT), st, scale));
+            bool tiled = false;
             if constexpr (!EXACT) {
-                if (p.sat) {
-                    const int64_t cnt = p.Q * p.n * p.d;
+                if (p.sat) {  // tile-major scaled copies; envelopes as (midpoint, inflated half width)
+                    tiled = true;
+                    const int rows = p.n * p.d;
+                    TRY(planarize_tiled(at<float>(ws, p.o_up), p.Q, rows, at<float>(ws, p.o_upT), st, scale));
+                    TRY(planarize_tiled(at<float>(ws, p.o_lo), p.Q, rows, at<float>(ws, p.o_loT), st, scale));
+                    TRY(planarize_tiled((const float*)queries, p.Q, rows, at<float>(ws, p.o_qT), st, scale));
+                    if (!p.cand_planar)
+                        TRY(planarize_tiled((const float*)cands, p.N, rows, at<float>(ws, p.o_candT), st, scale));
+                    const int64_t cnt = planar_pad(p.Q) * rows;
                     midhalf_kernel<<<grid_for(cnt, 256), 256, 0, st>>>(at<float>(ws, p.o_upT), at<float>(ws, p.o_loT),
-                                                                        cnt, scale);
+                                                                        cnt);
                     TRY(launch_status());
                 }
+            }
+            if (!tiled) {
+                TRY(planarize<T>(at<T>(ws, p.o_up), p.Q, p.n * p.d, at<T>(ws, p.o_upT), st));
+                TRY(planarize<T>(at<T>(ws, p.o_lo), p.Q, p.n * p.d, at<T>(ws, p.o_loT), st));
+                TRY(planarize<T>((const T*)queries, p.Q, p.n * p.d, at<T>(ws, p.o_qT), st));
+                if (!p.cand_planar) TRY(planarize<T>((const T*)cands, p.N, p.n * p.d, at<T>(ws, p.o_candT), st));
             }
         }
         if (!EXACT) {
