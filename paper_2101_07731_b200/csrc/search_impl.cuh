@@ -310,7 +310,7 @@ __device__ __forceinline__ void mv_bar_wait(uint64_t* bar, unsigned parity) {
 // DX > 0: the dimension count is a compile-time constant (fully unrolled
 // per-dimension loop for the hot shapes); DX == 0: runtime d.
 template <typename T, int DMAX, bool EXACT, bool UB, int DX, bool SAT>
-__global__ void __launch_bounds__(256) lbmv_matrix_kernel(const T* __restrict__ UT, const T* __restrict__ LT,
+__global__ void __launch_bounds__(256, (SAT && DX > 0 && DX <= 8) ? 3 : 1) lbmv_matrix_kernel(const T* __restrict__ UT, const T* __restrict__ LT,
                                                           const T* __restrict__ QTP, const T* __restrict__ CT_,
                                                           int64_t Q, int64_t N, int n, int d, int TC,
                                                           T* __restrict__ out, T* __restrict__ ub_out, int ub_stride,
@@ -591,7 +591,10 @@ int launch_lbmv_matrix(const T* UT, const T* LT, const T* QTP, const T* CT, int6
     const bool ub = ub_out != nullptr;
     // two staging buffers of TC time steps each (layout us | ls | cs | qs)
     const size_t per_t = (size_t)d * (3 * Tile::QT + Tile::CT) * sizeof(T);
-    int TC = (int)((96 * 1024) / (2 * per_t));
+    // SAT with a compile-time d <= 8: three blocks per SM (80 registers by launch bounds), so 72 KB of
+    // staging each (C4 LB_MV 99.3 -> 93.8 ms per 1k queries; d = 20 spills at 80 registers and keeps two)
+    const bool three = scale != nullptr && (d == 3 || d == 4 || d == 5 || d == 6 || d == 8) && d <= DMAX;
+    int TC = (int)(((three ? 72 : 96) * 1024) / (2 * per_t));
     TC = TC < 1 ? 1 : (TC > 16 ? 16 : TC);
     TC = TC > n ? n : TC;
     const size_t smem = 2 * per_t * TC + 16;  // + the two mbarriers of the TMA staging
