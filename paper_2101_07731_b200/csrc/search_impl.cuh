@@ -561,7 +561,10 @@ __device__ __forceinline__ void lbmv_matrix_kernel_body(const T* __restrict__ UT
 #pragma unroll
             for (int j = 0; j < M; ++j) {
                 total[i][j] *= inv;
-                if constexpr (UB) ubt[i][j] *= inv;
+                // the upper bound seeds d_best directly (topk_kernel): a term whose scaled
+                // square sum is subnormal is flushed by sqrt.approx.ftz, losing < 2^-63 --
+                // give it back so the seed never falls below the path's cost
+                if constexpr (UB) ubt[i][j] = (ubt[i][j] + (T)n * (T)0x1p-62) * inv;
             }
     }
 #pragma unroll

@@ -295,7 +295,7 @@ def test_edge_cases(P, rng):
 
 
 
-@pytest.mark.parametrize("case", ["offset", "outside", "tiny", "huge", "ulps", "mixed_scale"])
+@pytest.mark.parametrize("case", ["offset", "outside", "tiny", "huge", "ulps", "mixed_scale", "dead_sensor"])
 def test_saturating_lb_mv_adversarial(P, rng, case):
     """float32 searches prune on the saturating LB_MV pass (scaled planar
     operands, midpoint / inflated half-width envelopes, FADD.SAT): inputs
@@ -330,6 +330,14 @@ def test_saturating_lb_mv_adversarial(P, rng, case):
                                      np.where(steps < 0, np.nextafter(moved, np.float32(-np.inf)), moved))
                 cands[100 + 8 * j + k] = moved
         cands[300:308] = cands[:8]  # exact duplicates: the lower index wins
+    elif case == "dead_sensor":
+        # near-zero series inside a collection of range ~1e6: their differences vanish in the
+        # scaled domain (the seed upper bound must not fall to 0) but not in the DTW's float32
+        cands = walk * 3e4
+        cands[50:90] = 1e-14 * rng.normal(size=(40, n, d))
+        cands[60] = 0.0
+        queries = 1e-14 * rng.normal(size=(8, n, d))
+        queries[1] = cands[70] * 0.5
     else:  # mixed_scale
         sc = np.array([1e-3, 1.0, 1e3, 1e-6, 30.0, 1e5])
         cands, queries = walk * sc, queries * sc
