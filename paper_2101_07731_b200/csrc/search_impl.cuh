@@ -1935,14 +1935,15 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     // qx: the column's 2*DP words; pk: band slot s.  With `full`, every row is
     // inside the band and row 0's upper neighbour (slot s+1) exists; otherwise
     // s is a compile-time constant after unrolling and the checks fold.
-    auto iter = [&](int s, bool full, const float* qx, float* pk) {
-        float x[D];
+    auto load_x = [&](float (&x)[2 * DP], const float* qx) {
 #pragma unroll
         for (int pp = 0; pp < DP; ++pp) {
             const float2 v = *reinterpret_cast<const float2*>(qx + 2 * pp);
             x[2 * pp] = v.x;
-            if (2 * pp + 1 < D) x[2 * pp + 1] = v.y;
+            x[2 * pp + 1] = v.y;
         }
+    };
+    auto iter_x = [&](int s, bool full, const float (&x)[2 * DP], float* pk) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const bool active = full || (s - r >= 0 && s - r <= B - 1);
@@ -1977,6 +1978,11 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
             }
         }
     };
+    auto iter = [&](int s, bool full, const float* qx, float* pk) {
+        float x[2 * DP];
+        load_x(x, qx);
+        iter_x(s, full, x, pk);
+    };
     while (true) {
         if (head_h < 0) {
             refill();
@@ -2001,15 +2007,34 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
             } else {
                 pu = ps[j0 * R * 32];
             }
+            if constexpr (D <= 8) {
+                // the first column of a block is read one block ahead (its
+                // consumer was the step's largest stall site: 9% of the samples)
+                float xn[2 * DP];
+                load_x(xn, qg + (j0 > 1 ? j0 : 1) * QGS);
 #pragma unroll 1
-            for (int j = j0 > 1 ? j0 : 1; j <= JF; ++j) {
-                const float* qb = qg + j * QGS;
-                float* pb = ps + j * R * 32;
+                for (int j = j0 > 1 ? j0 : 1; j <= JF; ++j) {
+                    const float* qb = qg + j * QGS;
+                    float* pb = ps + j * R * 32;
+                    iter_x(j * R, true, xn, pb);
+                    load_x(xn, qb + QGS);  // block j+1's (or the tail's) first column
 #pragma unroll
-                for (int t = 0; t < R; ++t) iter(j * R + t, true, qb + t * 2 * DP, pb + t * 32);
+                    for (int t = 1; t < R; ++t) iter(j * R + t, true, qb + t * 2 * DP, pb + t * 32);
+                }
+                iter_x(ST, false, xn, ps + ST * 32);
+#pragma unroll
+                for (int s = ST + 1; s < NIT; ++s) iter(s, false, qg + (s / R) * QGS + (s % R) * 2 * DP, ps + s * 32);
+            } else {  // wide points: no registers to spare for the read-ahead
+#pragma unroll 1
+                for (int j = j0 > 1 ? j0 : 1; j <= JF; ++j) {
+                    const float* qb = qg + j * QGS;
+                    float* pb = ps + j * R * 32;
+#pragma unroll
+                    for (int t = 0; t < R; ++t) iter(j * R + t, true, qb + t * 2 * DP, pb + t * 32);
+                }
+#pragma unroll
+                for (int s = ST; s < NIT; ++s) iter(s, false, qg + (s / R) * QGS + (s % R) * 2 * DP, ps + s * 32);
             }
-#pragma unroll
-            for (int s = ST; s < NIT; ++s) iter(s, false, qg + (s / R) * QGS + (s % R) * 2 * DP, ps + s * 32);
             // cascade: LB_MV terms of rows i..i+R-1 from the envelope group
             float bound = rmin;
             if (casc) {
