@@ -61,7 +61,7 @@ const char* dtw_kernel_name(const tcdtw_search_desc* dsc) {
     Plan p;
     if (make_plan(dsc, &p) != TCDTW_OK) return "invalid";
     if (!p.exact) {
-        const int r = laner_rows_shape(p.n, p.d, p.B);
+        const int r = laner_any_rows_shape(p.n, p.d, p.B);
         if (r == 4) return "dtw_laner_kernel<R=4>";
         if (r == 2) return "dtw_laner_kernel<R=2>";
     }

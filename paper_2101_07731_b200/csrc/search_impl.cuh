@@ -1697,21 +1697,31 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                                                              float* __restrict__ res, int* __restrict__ tile_ctr) {
     n_tiles = tile_count(tl, n_tiles);
     using L = LaneRLayout<D, R>;
-    constexpr int W = (B - 1) / 2, DP = L::DP, QGS = L::QGS, EGS = L::EGS, EQ = L::EQ, RD = R * D;
-    constexpr int NIT = B + R - 1;              // iterations per step
-    constexpr int JF = (B - 1 - R) / R;         // full blocks j = 1..JF (all rows inside the band)
-    constexpr int ST = R * (JF + 1);            // first tail iteration
+    constexpr int DP = L::DP, QGS = L::QGS, EGS = L::EGS, EQ = L::EQ, RD = R * D;
+    // B == 0: the band is a run-time value with 2W % R == 0 (any even W for
+    // R = 4, any W for R = 2): one instantiation per (D, R) serves every such
+    // window.  The step is prologue (R iterations), JF full blocks and a
+    // tail of R iterations whose active-row pattern (tail iteration u: rows
+    // r >= u) does not depend on W; PB is a stand-in band with that pattern
+    // for the compile-time tests of the tail.  B > 0: everything folds.
+    constexpr bool RT = (B == 0);
+    constexpr int PB = RT ? 4 * R + 1 : B;
+    constexpr int PST = R * ((PB - 1 - R) / R + 1), NTAIL = PB + R - 1 - PST;
+    const int Bv = RT ? 2 * a.w + 1 : B;
+    const int W = (Bv - 1) / 2;
+    const int JF = (Bv - 1 - R) / R;            // full blocks j = 1..JF (all rows inside the band)
+    const int ST = R * (JF + 1);                // first tail iteration
     // Head batches: the first HS steps of a pair (rows 0 .. R*HS-1) start at
     // iteration s0 = W - i >= R (earlier columns are < 0), rounded down to a
     // whole block (j0 = s0 / R).  A warp runs them in lockstep for up to 32
     // fresh pairs, so the trimmed iterations are skipped by the whole warp.
-    constexpr int HS = (W >= R) ? W / R : 0;
-    static_assert(B >= R + 1 && JF >= 1, "band too narrow for R rows per step");
+    const int HS = (W >= R) ? W / R : 0;
+    static_assert(RT || (B >= R + 1 && (B - 1 - R) / R >= 1), "band too narrow for R rows per step");
     extern __shared__ __align__(16) float smem_f[];
     const int n = a.n;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int qrows = a.qpad_rows;
-    float* const qs = smem_f + (size_t)wib * L::warp_words(n, qrows, B);  // query groups
+    float* const qs = smem_f + (size_t)wib * L::warp_words(n, qrows, Bv);  // query groups
     float* const es = qs + L::q_words(qrows);                              // envelope groups
     float* const ps = es + L::e_words(n) + lane;                           // band row: slot k at ps[k*32]
     const unsigned FULL = 0xffffffffu;
@@ -1719,16 +1729,16 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     const int thr_mask = a.thr_every - 1;
     const bool casc = CASC && a.lb != nullptr && a.abandon && a.env_up != nullptr && a.cascade;
     const bool heads = HS > 0 && n > R * (HS + 1) && a.lane_scratch != nullptr;
-    float* const scr = a.lane_scratch + (size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * laner_scratch_words(B);
+    float* const scr = a.lane_scratch + (size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * laner_scratch_words(Bv);
     // queued pairs (slot = the lane that ran them): band row, result entry,
     // LB_MV total and cascade prefix in scratch; the candidate and the next
     // row stay in that lane's registers q_cand / q_i (the pop's row loads
     // depend on them)
     float* const q_band = scr;
-    int* const q_el = reinterpret_cast<int*>(scr + 32 * B);
+    int* const q_el = reinterpret_cast<int*>(scr + 32 * Bv);
     int* const q_eh = q_el + 32;
-    float* const q_lb = scr + 32 * B + 64;
-    float* const q_pre = scr + 32 * B + 96;
+    float* const q_lb = scr + 32 * Bv + 64;
+    float* const q_pre = scr + 32 * Bv + 96;
     // warp-uniform work state: current tile, reservoir window, query in smem
     int64_t t_begin = 0;
     int t_q = -1, t_len = 0, t_next = 0, r_base = 0, slot_q = -1;
@@ -1814,7 +1824,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
         thr = a.abandon ? scale_up<float>(t_thr_raw, a.mg) : INF;
         thr_pend_raw = t_thr_raw;
 #pragma unroll
-        for (int k = 0; k < B; ++k) ps[k * 32] = (k == W) ? 0.f : INF;
+        for (int k = 0; k < Bv; ++k) ps[k * 32] = (k == W) ? 0.f : INF;
         load_rows(c, cc, 0);
         i = 0;
     };
@@ -1862,7 +1872,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                     lbtot = q_lb[sl];
                     prefix = q_pre[sl];
 #pragma unroll
-                    for (int k = 0; k < B; ++k) ps[k * 32] = q_band[k * 32 + sl];
+                    for (int k = 0; k < Bv; ++k) ps[k * 32] = q_band[k * 32 + sl];
                     const float raw = a.abandon ? load_volatile(a.thr_src + slot_q) : INF;
                     thr = a.abandon ? scale_up<float>(raw, a.mg) : INF;
                     thr_pend_raw = raw;
@@ -1897,7 +1907,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                     q_lb[lane] = lbtot;
                     q_pre[lane] = prefix;
 #pragma unroll
-                    for (int k = 0; k < B; ++k) q_band[k * 32 + lane] = ps[k * 32];
+                    for (int k = 0; k < Bv; ++k) q_band[k * 32 + lane] = ps[k * 32];
                 }
                 __syncwarp();
                 i = -1;
@@ -1946,8 +1956,8 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     auto iter_x = [&](int s, bool full, const float (&x)[2 * DP], float* pk) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const bool active = full || (s - r >= 0 && s - r <= B - 1);
-            if (!active) {  // not started (all INF) or past slot B-1
+            const bool active = full || (s - r >= 0 && s - r <= PB - 1);
+            if (!active) {  // not started (all INF) or past the last slot
                 prv[r] = cur[r];
                 cur[r] = INF;
                 continue;
@@ -1962,7 +1972,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
             const float cost = fast_sqrt(acc);
             float up, dg;
             if (r == 0) {
-                up = (full || s + 1 <= B - 1) ? pk[32] : INF;
+                up = (full || s + 1 <= PB - 1) ? pk[32] : INF;
                 dg = pu;
                 pu = up;
             } else {
@@ -1991,7 +2001,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
         // head step h: rows i = R h .. with the first (W - i) / R blocks
         // skipped (their columns are < 0); body steps start at block 0
         const int j0 = head_h >= 0 ? (W - R * head_h) / R : 0;
-        c_issued += head_h >= 0 ? R * (B - R * j0) + R * (R - 1) / 2 : R * B;
+        c_issued += head_h >= 0 ? R * (Bv - R * j0) + R * (R - 1) / 2 : R * Bv;
         if (c_cells >= (1u << 30) || c_issued >= (1u << 30)) flush();
         if (i >= 0) {
             const bool more = i + R < n;
@@ -2021,9 +2031,10 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
 #pragma unroll
                     for (int t = 1; t < R; ++t) iter(j * R + t, true, qb + t * 2 * DP, pb + t * 32);
                 }
-                iter_x(ST, false, xn, ps + ST * 32);
+                iter_x(PST, false, xn, ps + ST * 32);
 #pragma unroll
-                for (int s = ST + 1; s < NIT; ++s) iter(s, false, qg + (s / R) * QGS + (s % R) * 2 * DP, ps + s * 32);
+                for (int u = 1; u < NTAIL; ++u)
+                    iter(PST + u, false, qg + (ST / R + u / R) * QGS + (u % R) * 2 * DP, ps + (ST + u) * 32);
             } else {  // wide points: no registers to spare for the read-ahead
 #pragma unroll 1
                 for (int j = j0 > 1 ? j0 : 1; j <= JF; ++j) {
@@ -2033,7 +2044,8 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                     for (int t = 0; t < R; ++t) iter(j * R + t, true, qb + t * 2 * DP, pb + t * 32);
                 }
 #pragma unroll
-                for (int s = ST; s < NIT; ++s) iter(s, false, qg + (s / R) * QGS + (s % R) * 2 * DP, ps + s * 32);
+                for (int u = 0; u < NTAIL; ++u)
+                    iter(PST + u, false, qg + (ST / R + u / R) * QGS + (u % R) * 2 * DP, ps + (ST + u) * 32);
             }
             // cascade: LB_MV terms of rows i..i+R-1 from the envelope group
             float bound = rmin;
@@ -2100,6 +2112,8 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
 #define TCDTW_LANER_SPECS(X)                                                                          \
     X(3, 25, 4) X(4, 25, 4) X(5, 25, 4) X(6, 25, 4) X(8, 25, 4) X(3, 13, 4) X(4, 13, 4) X(5, 13, 4) \
     X(6, 13, 4) X(8, 13, 4) X(20, 13, 2) X(5, 103, 4)
+// run-time band (B = 0): (d, rows per step); served when 2W % R == 0, W >= R
+#define TCDTW_LANER_RT_SPECS(X) X(3, 4) X(4, 4) X(5, 4) X(6, 4) X(8, 4) X(4, 2) X(6, 2) X(8, 2) X(20, 2)
 
 static int laner_rows_shape(int n, int d, int B) {  // rows per step for this shape, 0 = not served
     int rows = 0;
@@ -2110,9 +2124,30 @@ static int laner_rows_shape(int n, int d, int B) {  // rows per step for this sh
     return rows;
 }
 
+// The run-time-band instantiation for a shape without a compiled band: rows
+// per step (4 preferred), 0 = none.  Needs n % R == 0, W >= R, 2W % R == 0
+// and at least three blocks per SM of shared memory (query + envelope + band
+// row per warp); longer bands go to the wavefront kernels.
+static int laner_rt_rows_shape(int n, int d, int B) {
+    if (laner_rows_shape(n, d, B) > 0 || B < 3) return 0;
+    const int W = (B - 1) / 2, qrows = n + 2 * W + 8;
+    int rows = 0;
+#define TCDTW_LANER_RT_OK(DD, RR)                                                                         \
+    if (rows == 0 && d == DD && n % RR == 0 && W >= RR && (2 * W) % RR == 0 &&                            \
+        (size_t)2 * LaneRLayout<DD, RR>::warp_words(n, qrows, B) * sizeof(float) <= 76 * 1024)           \
+        rows = RR;
+    TCDTW_LANER_RT_SPECS(TCDTW_LANER_RT_OK)
+#undef TCDTW_LANER_RT_OK
+    return rows;
+}
+static int laner_any_rows_shape(int n, int d, int B) {
+    const int r = laner_rows_shape(n, d, B);
+    return r > 0 ? r : laner_rt_rows_shape(n, d, B);
+}
+
 static int laner_rows(const SArgs<float>& a, int d, int B) {
     if (a.qpad == nullptr || (reinterpret_cast<uintptr_t>(a.cands) % 16) != 0) return 0;
-    return laner_rows_shape(a.n, d, B);
+    return laner_any_rows_shape(a.n, d, B);
 }
 
 #ifndef TCDTW_LANER_MINB
@@ -2151,6 +2186,14 @@ static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n
     }
     TCDTW_LANER_SPECS(TCDTW_LANER_CASE)
 #undef TCDTW_LANER_CASE
+    const int rt = laner_rt_rows_shape(a.n, d, B);
+#define TCDTW_LANER_RT_CASE(DD, RR)                                                           \
+    if (d == DD && rt == RR) {                                                                \
+        const int ww = LaneRLayout<DD, RR>::warp_words(a.n, a.qpad_rows, B);                  \
+        return go(dtw_laner_kernel<DD, 0, RR, true, TCDTW_LANER_MINB>, ww);                   \
+    }
+    TCDTW_LANER_RT_SPECS(TCDTW_LANER_RT_CASE)
+#undef TCDTW_LANER_RT_CASE
     return TCDTW_NOT_SUPPORTED;
 }
 
@@ -3514,7 +3557,7 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     const bool ti = dsc->method == TCDTW_METHOD_LB_TI ||
                     (dsc->method == TCDTW_METHOD_TC_DTW && dsc->advanced == TCDTW_METHOD_LB_TI);
     p.o_tisc = take(ti ? (size_t)p.adv_warps * 32 * 3 * p.B * es : 0);
-    p.o_lanesc = take(!p.exact && laner_rows_shape(p.n, p.d, p.B) > 0
+    p.o_lanesc = take(!p.exact && laner_any_rows_shape(p.n, p.d, p.B) > 0
                           ? (size_t)kLanerMaxWarps * laner_scratch_words(p.B) * sizeof(float) : 0);
     p.o_q32 = take(p.f32f ? series_q : 0);
     p.o_c32 = take(p.f32f ? (size_t)N * p.n * p.d * 4 : 0);
@@ -3630,7 +3673,7 @@ static SArgs<T> make_args(const tcdtw_search_desc* dsc, const Plan& p, const voi
     a.qpad_rows = p.qpad_rows;
     a.mg.add = nullptr;
     a.xq = a.xc = nullptr;
-    a.lane_scratch = (!p.exact && laner_rows_shape(p.n, p.d, p.B) > 0) ? at<float>(ws, p.o_lanesc) : nullptr;
+    a.lane_scratch = (!p.exact && laner_any_rows_shape(p.n, p.d, p.B) > 0) ? at<float>(ws, p.o_lanesc) : nullptr;
     a.cbox_lo = p.rev_pc ? (const T*)dsc->cand_box_lo : nullptr;
     a.cbox_hi = p.rev_pc ? (const T*)dsc->cand_box_hi : nullptr;
     if (p.f32f) {  // queries / cands are the float32 copies in the workspace

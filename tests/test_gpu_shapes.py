@@ -1,5 +1,6 @@
 """Search parity over a spread of shapes, so that every DTW kernel the
-dispatcher can pick (R-row lane kernel for its compiled shapes, two-row lane
+dispatcher can pick (R-row lane kernel for its compiled shapes and with a
+run-time band, two-row lane
 kernel, thread-per-pair, compile-time-d wavefront, generic wavefront,
 few-pairs path) is checked against the oracle, in float32 and float64."""
 
@@ -12,6 +13,9 @@ SHAPES = [  # (n, d, W)
     (1, 3, 0), (2, 1, 1), (7, 2, 3), (16, 4, 6), (33, 7, 5), (64, 20, 6), (64, 6, 12), (100, 9, 10),
     (128, 6, 12), (128, 5, 51), (128, 3, 6), (128, 8, 12), (200, 12, 40), (64, 32, 3), (96, 16, 30),
     (256, 5, 12), (130, 6, 12), (48, 24, 48),
+    # run-time-band lane kernel (no compiled (d, 2W+1) bucket): even W -> 4 rows per step, odd W -> 2
+    (128, 6, 10), (128, 6, 16), (128, 6, 11), (64, 20, 4), (256, 6, 24), (96, 4, 7), (128, 8, 30), (64, 3, 8),
+    (100, 5, 6), (128, 4, 4), (128, 6, 2),
 ]
 
 
