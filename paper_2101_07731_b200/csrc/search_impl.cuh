@@ -920,7 +920,8 @@ struct SArgs {
     int refill_min;  // lane kernel: refill once at least this many lanes are free
     int thr_every;   // lane kernels: re-read the live d_best every this many rows
     // float32: queries as coordinate pairs with W INF columns before and
-    // W + 8 after, (Q, qpad_rows, (d+1)/2) float2, staged by the R-row lane kernel
+    // W + 8 after, (Q, qpad_rows, (D+1)/2) float2 with D the lane kernel's dimension count
+    // (>= d, zero-padded), staged by the R-row lane kernel
     const float2* qpad;
     int qpad_rows;
     // TCDTW_FLAG_F32_FILTER: the float64 inputs the finalists are re-scored
@@ -1657,8 +1658,8 @@ static int launch_lane(const SArgs<T>& a, int d, int B, Tiles tl, int64_t n_tile
 // a pad that makes the group an odd number of 16-byte bank quads, so lanes
 // on different rows read shared memory with few conflicts.
 static __global__ void qpad_kernel(const float* __restrict__ q, int64_t Q, int n, int d, int w, int rows,
-                                   float2* __restrict__ out) {
-    const int DP = (d + 1) / 2;
+                                   float2* __restrict__ out, int dpad) {
+    const int DP = (dpad + 1) / 2;  // dpad >= d: the lane kernel's compile-time dimension count
     const int64_t tot = Q * rows * DP;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
         const int pp = (int)(e % DP);
@@ -1667,7 +1668,7 @@ static __global__ void qpad_kernel(const float* __restrict__ q, int64_t Q, int n
         float2 v = make_float2(dev_inf<float>(), dev_inf<float>());
         if (col >= 0 && col < n) {
             const float* src = q + (qi * n + col) * d;
-            v.x = src[2 * pp];
+            v.x = (2 * pp < d) ? src[2 * pp] : 0.f;
             v.y = (2 * pp + 1 < d) ? src[2 * pp + 1] : 0.f;
         }
         out[e] = v;
@@ -1772,15 +1773,29 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
         }
         c_comp = c_cells = c_issued = 0;
     };
+    // a.d < D: the series have fewer dimensions than the instantiation; the
+    // missing ones read as 0 on both sides (they add nothing to a distance or
+    // an envelope deviation, so every result is unchanged)
+    // (run-time-band instantiations only: the compiled buckets keep dd == D
+    // a compile-time fact -- the test cost C4 1% of its DTW time)
+    const int dd = (B == 0) ? a.d : D;
     auto load_rows = [&](float (&dst)[RD], uint32_t cc, int row) {  // rows row..row+R-1, row % R == 0
-        const float4* src = reinterpret_cast<const float4*>(a.cands + ((int64_t)cc * n + row) * D);
+        if (dd == D) {
+            const float4* src = reinterpret_cast<const float4*>(a.cands + ((int64_t)cc * n + row) * D);
 #pragma unroll
-        for (int v = 0; v < RD / 4; ++v) {
-            const float4 x = __ldg(src + v);
-            dst[4 * v] = x.x;
-            dst[4 * v + 1] = x.y;
-            dst[4 * v + 2] = x.z;
-            dst[4 * v + 3] = x.w;
+            for (int v = 0; v < RD / 4; ++v) {
+                const float4 x = __ldg(src + v);
+                dst[4 * v] = x.x;
+                dst[4 * v + 1] = x.y;
+                dst[4 * v + 2] = x.z;
+                dst[4 * v + 3] = x.w;
+            }
+        } else {
+            const float* src = a.cands + ((int64_t)cc * n + row) * dd;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int p = 0; p < D; ++p) dst[r * D + p] = p < dd ? __ldg(src + r * dd + p) : 0.f;
         }
     };
     auto load_reservoir = [&]() {  // entries r_base .. r_base+31 of the tile, one per lane
@@ -1800,13 +1815,13 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
             *reinterpret_cast<float2*>(qs + (col / R) * QGS + (col % R) * 2 * DP + 2 * pp) = src[e];
         }
         if (casc) {
-            const float* eu = a.env_up + (int64_t)q * n * D;
-            const float* el = a.env_lo + (int64_t)q * n * D;
+            const float* eu = a.env_up + (int64_t)q * n * dd;
+            const float* el = a.env_lo + (int64_t)q * n * dd;
             for (int e = lane; e < n * D; e += 32) {
                 const int row = e / D, p = e - (e / D) * D;
                 float* g = es + (row / R) * EGS + (row % R) * D + p;
-                g[0] = eu[e];
-                g[4 * EQ] = el[e];
+                g[0] = p < dd ? eu[row * dd + p] : 0.f;
+                g[4 * EQ] = p < dd ? el[row * dd + p] : 0.f;
             }
         }
         slot_q = q;
@@ -2113,37 +2128,46 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     X(3, 25, 4) X(4, 25, 4) X(5, 25, 4) X(6, 25, 4) X(8, 25, 4) X(3, 13, 4) X(4, 13, 4) X(5, 13, 4) \
     X(6, 13, 4) X(8, 13, 4) X(20, 13, 2) X(5, 103, 4)
 // run-time band (B = 0): (d, rows per step); served when 2W % R == 0, W >= R
-#define TCDTW_LANER_RT_SPECS(X) X(3, 4) X(4, 4) X(5, 4) X(6, 4) X(8, 4) X(4, 2) X(6, 2) X(8, 2) X(20, 2)
+#define TCDTW_LANER_RT_SPECS(X) \
+    X(3, 4) X(4, 4) X(5, 4) X(6, 4) X(8, 4) X(4, 2) X(6, 2) X(8, 2) X(12, 2) X(16, 2) X(20, 2)
 
-static int laner_rows_shape(int n, int d, int B) {  // rows per step for this shape, 0 = not served
-    int rows = 0;
+// The lane-kernel instantiation serving a shape: compile-time dimension
+// count DD, rows per step, and whether the band is compiled (the (d, 2W+1,
+// R) buckets, exact d) or a run-time value (DD >= d, missing dimensions
+// zero-padded on the fly).  The smallest DD wins, then a compiled band, then
+// 4 rows.
+// A run-time band needs n % R == 0, W >= R, 2W % R == 0 and at least three
+// blocks per SM of shared memory (query + envelope + band row per warp);
+// longer bands go to the wavefront kernels.
+struct LanerPick {
+    int dims = 0, rows = 0;
+    bool rt = false;
+};
+static LanerPick laner_pick(int n, int d, int B) {
+    LanerPick best;
+    auto better = [&](int DD, int RR, bool rt) {
+        if (best.dims == 0) return true;
+        if (DD != best.dims) return DD < best.dims;
+        if (rt != best.rt) return !rt;
+        return RR > best.rows;
+    };
 #define TCDTW_LANER_OK(DD, BB, RR) \
-    if (d == DD && B == BB && n % RR == 0) rows = RR;
+    if (DD == d && B == BB && n % RR == 0 && better(DD, RR, false)) best = LanerPick{DD, RR, false};
     TCDTW_LANER_SPECS(TCDTW_LANER_OK)
 #undef TCDTW_LANER_OK
-    return rows;
-}
-
-// The run-time-band instantiation for a shape without a compiled band: rows
-// per step (4 preferred), 0 = none.  Needs n % R == 0, W >= R, 2W % R == 0
-// and at least three blocks per SM of shared memory (query + envelope + band
-// row per warp); longer bands go to the wavefront kernels.
-static int laner_rt_rows_shape(int n, int d, int B) {
-    if (laner_rows_shape(n, d, B) > 0 || B < 3) return 0;
-    const int W = (B - 1) / 2, qrows = n + 2 * W + 8;
-    int rows = 0;
+    if (B >= 3) {
+        const int W = (B - 1) / 2, qrows = n + 2 * W + 8;
 #define TCDTW_LANER_RT_OK(DD, RR)                                                                         \
-    if (rows == 0 && d == DD && n % RR == 0 && W >= RR && (2 * W) % RR == 0 &&                            \
-        (size_t)2 * LaneRLayout<DD, RR>::warp_words(n, qrows, B) * sizeof(float) <= 76 * 1024)           \
-        rows = RR;
-    TCDTW_LANER_RT_SPECS(TCDTW_LANER_RT_OK)
+    if (DD >= d && n % RR == 0 && W >= RR && (2 * W) % RR == 0 &&                                         \
+        (size_t)2 * LaneRLayout<DD, RR>::warp_words(n, qrows, B) * sizeof(float) <= 76 * 1024 &&         \
+        better(DD, RR, true))                                                                             \
+        best = LanerPick{DD, RR, true};
+        TCDTW_LANER_RT_SPECS(TCDTW_LANER_RT_OK)
 #undef TCDTW_LANER_RT_OK
-    return rows;
+    }
+    return best;
 }
-static int laner_any_rows_shape(int n, int d, int B) {
-    const int r = laner_rows_shape(n, d, B);
-    return r > 0 ? r : laner_rt_rows_shape(n, d, B);
-}
+static int laner_any_rows_shape(int n, int d, int B) { return laner_pick(n, d, B).rows; }
 
 static int laner_rows(const SArgs<float>& a, int d, int B) {
     if (a.qpad == nullptr || (reinterpret_cast<uintptr_t>(a.cands) % 16) != 0) return 0;
@@ -2179,16 +2203,16 @@ static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n
     };
     // new pairs load their first rows themselves (no register prefetch in
     // the reservoir): 126 registers at d=6, 16 warps per SM
+    const LanerPick pk = laner_pick(a.n, d, B);
 #define TCDTW_LANER_CASE(DD, BB, RR)                                                          \
-    if (d == DD && B == BB && a.n % RR == 0) {                                                \
+    if (!pk.rt && pk.dims == DD && B == BB && pk.rows == RR) {                                \
         const int ww = LaneRLayout<DD, RR>::warp_words(a.n, a.qpad_rows, BB);                 \
-        return go(dtw_laner_kernel<DD, BB, RR, true, TCDTW_LANER_MINB>, ww);                                 \
+        return go(dtw_laner_kernel<DD, BB, RR, true, TCDTW_LANER_MINB>, ww);                  \
     }
     TCDTW_LANER_SPECS(TCDTW_LANER_CASE)
 #undef TCDTW_LANER_CASE
-    const int rt = laner_rt_rows_shape(a.n, d, B);
 #define TCDTW_LANER_RT_CASE(DD, RR)                                                           \
-    if (d == DD && rt == RR) {                                                                \
+    if (pk.rt && pk.dims == DD && pk.rows == RR) {                                            \
         const int ww = LaneRLayout<DD, RR>::warp_words(a.n, a.qpad_rows, B);                  \
         return go(dtw_laner_kernel<DD, 0, RR, true, TCDTW_LANER_MINB>, ww);                   \
     }
@@ -3425,7 +3449,7 @@ struct Plan {
     size_t o_up, o_lo, o_upT, o_loT, o_candT, o_steps, o_blo, o_bhi, o_bcnt, o_lb, o_seed, o_seedres,
         o_seedcnt, o_dbest, o_ccnt, o_coff, o_surv, o_res, o_tcnt, o_toff, o_tq, o_tb, o_tl, o_sq, o_sb, o_sl,
         o_ctr, o_minv, o_min64, o_bidx, o_tctr, o_cub, o_fsc, o_tisc, o_qpad, o_cupT, o_cloT, o_lb2, total;
-    int qpad_rows;
+    int qpad_rows, qpad_dims;
     size_t cub_bytes;
     int fin_threads, adv_warps;
 };
@@ -3563,7 +3587,11 @@ static int make_plan(const tcdtw_search_desc* dsc, Plan* P) {
     p.o_c32 = take(p.f32f ? (size_t)N * p.n * p.d * 4 : 0);
     p.o_slack = take(p.f32f ? 32 : 0);
     p.qpad_rows = p.n + 2 * p.w + 8;
-    p.o_qpad = take(p.exact ? 0 : (size_t)Q * p.qpad_rows * ((p.d + 1) / 2) * 8);
+    {  // the lane kernel's compile-time dimension count for this shape (>= d), else d
+        const int ld = p.exact ? 0 : laner_pick(p.n, p.d, p.B).dims;
+        p.qpad_dims = ld > 0 ? ld : p.d;
+    }
+    p.o_qpad = take(p.exact ? 0 : (size_t)Q * p.qpad_rows * ((p.qpad_dims + 1) / 2) * 8);
     p.total = o;
     return TCDTW_OK;
 }
@@ -3884,10 +3912,10 @@ struct SearchImpl {
             }
         }
         if (!EXACT) {
-            const int DPq = (p.d + 1) / 2;
+            const int DPq = (p.qpad_dims + 1) / 2;
             const int64_t tot = p.Q * p.qpad_rows * DPq;
             qpad_kernel<<<grid_for(tot, 256), 256, 0, st>>>((const float*)queries, p.Q, p.n, p.d, p.w, p.qpad_rows,
-                                                             const_cast<float2*>(a.qpad));
+                                                             const_cast<float2*>(a.qpad), p.qpad_dims);
             TRY(launch_status());
         }
         if (a.adv == TCDTW_METHOD_LB_PC)

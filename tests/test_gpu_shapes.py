@@ -16,6 +16,9 @@ SHAPES = [  # (n, d, W)
     # run-time-band lane kernel (no compiled (d, 2W+1) bucket): even W -> 4 rows per step, odd W -> 2
     (128, 6, 10), (128, 6, 16), (128, 6, 11), (64, 20, 4), (256, 6, 24), (96, 4, 7), (128, 8, 30), (64, 3, 8),
     (100, 5, 6), (128, 4, 4), (128, 6, 2),
+    # dimension counts between the compiled ones: zero-padded on the fly to the next instantiation
+    (128, 7, 12), (128, 2, 12), (128, 1, 6), (64, 16, 6), (64, 13, 6), (128, 12, 12), (64, 9, 5), (128, 7, 10),
+    (64, 19, 6),
 ]
 
 
