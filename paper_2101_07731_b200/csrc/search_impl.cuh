@@ -1699,14 +1699,15 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     n_tiles = tile_count(tl, n_tiles);
     using L = LaneRLayout<D, R>;
     constexpr int DP = L::DP, QGS = L::QGS, EGS = L::EGS, EQ = L::EQ, RD = R * D;
-    // B == 0: the band is a run-time value with 2W % R == 0 (any even W for
-    // R = 4, any W for R = 2): one instantiation per (D, R) serves every such
-    // window.  The step is prologue (R iterations), JF full blocks and a
-    // tail of R iterations whose active-row pattern (tail iteration u: rows
-    // r >= u) does not depend on W; PB is a stand-in band with that pattern
-    // for the compile-time tests of the tail.  B > 0: everything folds.
-    constexpr bool RT = (B == 0);
-    constexpr int PB = RT ? 4 * R + 1 : B;
+    // B == 0 / B == 2: the band is a run-time value with 2W % R == B (even W
+    // / odd W for R = 4, any W for R = 2): one instantiation per (D, R, B)
+    // serves every such window.  The step is prologue (R iterations), JF full
+    // blocks and a tail of R + B iterations whose active-row pattern (tail
+    // iteration u: rows r >= u - B) does not depend on W; PB is a stand-in
+    // band with that pattern for the compile-time tests of the tail.
+    // B > 2: everything folds.
+    constexpr bool RT = (B == 0 || B == 2);   // B == 2: run-time band with 2W % R == 2 (odd W at R = 4)
+    constexpr int PB = RT ? 4 * R + 1 + B : B;
     constexpr int PST = R * ((PB - 1 - R) / R + 1), NTAIL = PB + R - 1 - PST;
     const int Bv = RT ? 2 * a.w + 1 : B;
     const int W = (Bv - 1) / 2;
@@ -1778,7 +1779,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     // an envelope deviation, so every result is unchanged)
     // (run-time-band instantiations only: the compiled buckets keep dd == D
     // a compile-time fact -- the test cost C4 1% of its DTW time)
-    const int dd = (B == 0) ? a.d : D;
+    const int dd = RT ? a.d : D;
     auto load_rows = [&](float (&dst)[RD], uint32_t cc, int row) {  // rows row..row+R-1, row % R == 0
         if (dd == D) {
             const float4* src = reinterpret_cast<const float4*>(a.cands + ((int64_t)cc * n + row) * D);
@@ -2127,16 +2128,17 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
 #define TCDTW_LANER_SPECS(X)                                                                          \
     X(3, 25, 4) X(4, 25, 4) X(5, 25, 4) X(6, 25, 4) X(8, 25, 4) X(3, 13, 4) X(4, 13, 4) X(5, 13, 4) \
     X(6, 13, 4) X(8, 13, 4) X(20, 13, 2) X(5, 103, 4)
-// run-time band (B = 0): (d, rows per step); served when 2W % R == 0, W >= R
-#define TCDTW_LANER_RT_SPECS(X) \
-    X(3, 4) X(4, 4) X(5, 4) X(6, 4) X(8, 4) X(4, 2) X(6, 2) X(8, 2) X(12, 2) X(16, 2) X(20, 2)
+// run-time band: (d, rows per step, 2W % R); served when W >= R
+#define TCDTW_LANER_RT_SPECS(X)                                                                  \
+    X(3, 4, 0) X(4, 4, 0) X(5, 4, 0) X(6, 4, 0) X(8, 4, 0) X(3, 4, 2) X(4, 4, 2) X(5, 4, 2) X(6, 4, 2) \
+    X(8, 4, 2) X(4, 2, 0) X(6, 2, 0) X(8, 2, 0) X(12, 2, 0) X(16, 2, 0) X(20, 2, 0)
 
 // The lane-kernel instantiation serving a shape: compile-time dimension
 // count DD, rows per step, and whether the band is compiled (the (d, 2W+1,
 // R) buckets, exact d) or a run-time value (DD >= d, missing dimensions
 // zero-padded on the fly).  The smallest DD wins, then a compiled band, then
 // 4 rows.
-// A run-time band needs n % R == 0, W >= R, 2W % R == 0 and at least three
+// A run-time band needs n % R == 0, W >= R and at least three
 // blocks per SM of shared memory (query + envelope + band row per warp);
 // longer bands go to the wavefront kernels.
 struct LanerPick {
@@ -2157,8 +2159,8 @@ static LanerPick laner_pick(int n, int d, int B) {
 #undef TCDTW_LANER_OK
     if (B >= 3) {
         const int W = (B - 1) / 2, qrows = n + 2 * W + 8;
-#define TCDTW_LANER_RT_OK(DD, RR)                                                                         \
-    if (DD >= d && n % RR == 0 && W >= RR && (2 * W) % RR == 0 &&                                         \
+#define TCDTW_LANER_RT_OK(DD, RR, MM)                                                                     \
+    if (DD >= d && n % RR == 0 && W >= RR && (2 * W) % RR == MM &&                                        \
         (size_t)2 * LaneRLayout<DD, RR>::warp_words(n, qrows, B) * sizeof(float) <= 76 * 1024 &&         \
         better(DD, RR, true))                                                                             \
         best = LanerPick{DD, RR, true};
@@ -2211,10 +2213,10 @@ static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n
     }
     TCDTW_LANER_SPECS(TCDTW_LANER_CASE)
 #undef TCDTW_LANER_CASE
-#define TCDTW_LANER_RT_CASE(DD, RR)                                                           \
-    if (pk.rt && pk.dims == DD && pk.rows == RR) {                                            \
+#define TCDTW_LANER_RT_CASE(DD, RR, MM)                                                       \
+    if (pk.rt && pk.dims == DD && pk.rows == RR && (B - 1) % RR == MM) {                      \
         const int ww = LaneRLayout<DD, RR>::warp_words(a.n, a.qpad_rows, B);                  \
-        return go(dtw_laner_kernel<DD, 0, RR, true, TCDTW_LANER_MINB>, ww);                   \
+        return go(dtw_laner_kernel<DD, MM, RR, true, TCDTW_LANER_MINB>, ww);                  \
     }
     TCDTW_LANER_RT_SPECS(TCDTW_LANER_RT_CASE)
 #undef TCDTW_LANER_RT_CASE

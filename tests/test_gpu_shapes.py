@@ -18,7 +18,7 @@ SHAPES = [  # (n, d, W)
     (100, 5, 6), (128, 4, 4), (128, 6, 2),
     # dimension counts between the compiled ones: zero-padded on the fly to the next instantiation
     (128, 7, 12), (128, 2, 12), (128, 1, 6), (64, 16, 6), (64, 13, 6), (128, 12, 12), (64, 9, 5), (128, 7, 10),
-    (64, 19, 6),
+    (64, 19, 6), (256, 6, 25), (128, 3, 5), (128, 7, 13), (64, 8, 9),
 ]
 
 
