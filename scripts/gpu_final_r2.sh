@@ -1,10 +1,10 @@
 # Round-2 evidence pass: GPU suite, smoke, opt-in full parity, 2-rank sharded
 # bench (gloo, one GPU), per-config benches, default bench + reference arm,
 # launch list and full captures of the dominant kernels (summarised on the
-# box).  Outputs in gpurun_out/fin2_*; summaries are copied to profiles/.
+# box).  Outputs in gpurun_out/fin3_*; summaries are copied to profiles/.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-P=gpurun_out/fin2
+P=gpurun_out/fin3
 timeout 1500 python -m pytest tests -m gpu -x -q > ${P}_tests.log 2>&1; echo "exit=$?" >> ${P}_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${P}_smoke.log 2>&1; echo "exit=$?" >> ${P}_smoke.log
 timeout 1200 python bench.py > ${P}_bench.log 2>&1; echo "exit=$?" >> ${P}_bench.log
