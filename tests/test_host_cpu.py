@@ -246,3 +246,40 @@ def test_new_entry_points_validate_without_gpu():
     assert nb.value >= 8 * (2 << 10)
     assert L.tcdtw_normalize(None, 10, 6, None, None, None, None, None, 0, None) == 1
     assert L.tcdtw_normalize(None, 0, 6, None, None, None, None, None, 0, None) == 1
+
+
+def test_dtw_kernel_choice_by_shape():
+    """The lane kernel's shape coverage (host logic only: tcdtw_dtw_kernel_name
+    plans the search, no launch): compiled (d, 2W+1) buckets, run-time bands
+    (even W / odd W at 4 rows per step, 2 rows for n % 4 != 0 or d > 8),
+    dimension padding, and the shapes left to the other kernels."""
+    import ctypes
+
+    from paper_2101_07731_b200 import _lib
+
+    L = _lib.load_library()
+
+    def name(n, d, w, dtype=0, flags=0):
+        desc = _lib.SearchDesc(dtype=dtype, n=n, dims=d, window=w, method=1, advanced=0, refresh_period=5,
+                               quant_levels=2, max_boxes=6, group_width=6, trigger_ti=0.1, trigger_pc=0.1,
+                               min_cell_frac=1e-5, n_queries=64, n_candidates=10000, candidate_base=0, seeds=0,
+                               flags=flags)
+        return L.tcdtw_dtw_kernel_name(ctypes.byref(desc)).decode()
+
+    four, two = "dtw_laner_kernel<R=4>", "dtw_laner_kernel<R=2>"
+    assert name(128, 6, 12) == four  # C4: compiled bucket
+    assert name(64, 20, 6) == two  # C2: compiled bucket
+    assert name(256, 5, 51) == four  # C1b: compiled bucket
+    for w in (4, 10, 11, 16, 25):  # run-time band, even and odd W
+        assert name(128, 6, w) == four, w
+    assert name(126, 6, 12) == two  # n % 4 != 0
+    for d in (1, 2, 7):  # padded to 3 / 3 / 8 dimensions
+        assert name(128, d, 12) == four, d
+    for d in (9, 12, 13, 16, 19):  # padded to 12 / 16 / 20 dimensions at 2 rows per step
+        assert name(128, d, 12) == two, d
+    assert name(128, 6, 3) == two and name(128, 6, 1) not in (four, two)  # W >= rows per step
+    assert name(127, 6, 12) not in (four, two)  # odd n
+    assert name(128, 24, 12) not in (four, two)  # d > 20
+    assert name(1024, 8, 102) not in (four, two)  # C3's band row does not fit three blocks per SM
+    assert name(128, 6, 12, dtype=1) not in (four, two)  # float64 without the filter: exact kernels
+    assert name(128, 6, 12, dtype=1, flags=_lib.FLAG_F32_FILTER) == four
