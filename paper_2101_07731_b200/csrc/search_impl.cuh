@@ -1683,7 +1683,7 @@ struct LaneRLayout {
     static constexpr int EGS = 8 * EQ + 4;      // words per R-row envelope group: 2*EQ + 1 (odd) float4s
     static_assert((R * D) % 4 == 0, "R rows of D floats must be whole float4s");
     __host__ __device__ static int q_words(int qrows) { return (((qrows + R - 1) / R) * QGS + 3) & ~3; }
-    __host__ __device__ static int e_words(int n) { return n / R * EGS; }
+    __host__ __device__ static int e_words(int n) { return (n + R - 1) / R * EGS; }
     __host__ __device__ static int warp_words(int n, int qrows, int B) { return q_words(qrows) + e_words(n) + B * 32; }
 };
 
@@ -1780,8 +1780,12 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
     // (run-time-band instantiations only: the compiled buckets keep dd == D
     // a compile-time fact -- the test cost C4 1% of its DTW time)
     const int dd = RT ? a.d : D;
+    // n % R != 0 (run-time-band instantiations only): the pair's last n % R
+    // rows follow its last full step (tail rows, below); rows past n - 1 read
+    // as 0 and a row stride that breaks the 16-byte alignment goes scalar
+    const bool vec_rows = dd == D && (!RT || ((n * D) % 4 == 0));
     auto load_rows = [&](float (&dst)[RD], uint32_t cc, int row) {  // rows row..row+R-1, row % R == 0
-        if (dd == D) {
+        if (vec_rows && (!RT || row + R <= n)) {
             const float4* src = reinterpret_cast<const float4*>(a.cands + ((int64_t)cc * n + row) * D);
 #pragma unroll
             for (int v = 0; v < RD / 4; ++v) {
@@ -1796,7 +1800,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
 #pragma unroll
             for (int r = 0; r < R; ++r)
 #pragma unroll
-                for (int p = 0; p < D; ++p) dst[r * D + p] = p < dd ? __ldg(src + r * dd + p) : 0.f;
+                for (int p = 0; p < D; ++p) dst[r * D + p] = (p < dd && row + r < n) ? __ldg(src + r * dd + p) : 0.f;
         }
     };
     auto load_reservoir = [&]() {  // entries r_base .. r_base+31 of the tile, one per lane
@@ -2097,6 +2101,39 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
                 stop = i + R - 1;
                 abandoned = true;
             }
+            if constexpr (RT) {
+                if (stop < 0 && n - (i + R) < R) {
+                    // the pair's last n % R rows (in nc): one row at a time, in place in the
+                    // band row (slot k: diagonal = old slot k, up = old slot k+1, left = new
+                    // slot k-1); only DTWs that run to completion get here
+                    const int i2 = i + R, rem = n - i2;
+#pragma unroll
+                    for (int r = 0; r < R - 1; ++r) {
+                        if (r < rem) {
+                            float left = INF;
+                            for (int k = 0; k < Bv; ++k) {
+                                const int col = i2 + r + k;  // padded query column
+                                float x[2 * DP];
+                                load_x(x, qs + (col / R) * QGS + (col % R) * 2 * DP);
+                                float acc = 0.f;
+#pragma unroll
+                                for (int p = 0; p < D; ++p) {
+                                    const float df = nc[r * D + p] - x[p];
+                                    acc = fmaf(df, df, acc);
+                                }
+                                const float up = k + 1 < Bv ? ps[(k + 1) * 32] : INF;
+                                const float v = fast_sqrt(acc) + fminf(fminf(up, ps[k * 32]), left);
+                                ps[k * 32] = v;
+                                left = v;
+                            }
+                        }
+                    }
+                    c_issued += rem * Bv;
+                    stop = n - 1;
+                    fin = ps[W * 32];
+                    abandoned = fin > thr;  // dtw.py:101-102
+                }
+            }
             if (stop >= 0) {
                 res[ent] = abandoned ? INF : fin;
                 if (!abandoned) {
@@ -2138,7 +2175,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
 // R) buckets, exact d) or a run-time value (DD >= d, missing dimensions
 // zero-padded on the fly).  The smallest DD wins, then a compiled band, then
 // 4 rows.
-// A run-time band needs n % R == 0, W >= R and at least three
+// A run-time band needs W >= R, n >= 2R when n % R != 0 (tail rows) and at least three
 // blocks per SM of shared memory (query + envelope + band row per warp);
 // longer bands go to the wavefront kernels.
 struct LanerPick {
@@ -2160,7 +2197,7 @@ static LanerPick laner_pick(int n, int d, int B) {
     if (B >= 3) {
         const int W = (B - 1) / 2, qrows = n + 2 * W + 8;
 #define TCDTW_LANER_RT_OK(DD, RR, MM)                                                                     \
-    if (DD >= d && n % RR == 0 && W >= RR && (2 * W) % RR == MM &&                                        \
+    if (DD >= d && (n % RR == 0 || n >= 2 * RR) && W >= RR && (2 * W) % RR == MM &&                       \
         (size_t)2 * LaneRLayout<DD, RR>::warp_words(n, qrows, B) * sizeof(float) <= 76 * 1024 &&         \
         better(DD, RR, true))                                                                             \
         best = LanerPick{DD, RR, true};

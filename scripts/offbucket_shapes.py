@@ -20,7 +20,7 @@ from paper_2101_07731_b200 import datasets  # noqa: E402
 
 SHAPES = [  # (n, d, W)
     (128, 6, 12), (128, 7, 12), (128, 8, 12), (128, 6, 10), (128, 6, 16), (126, 6, 12), (128, 12, 12),
-    (128, 2, 12), (256, 6, 25), (64, 20, 6), (64, 16, 6),
+    (128, 2, 12), (256, 6, 25), (64, 20, 6), (64, 16, 6), (127, 6, 12),
 ]
 
 

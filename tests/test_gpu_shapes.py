@@ -19,6 +19,8 @@ SHAPES = [  # (n, d, W)
     # dimension counts between the compiled ones: zero-padded on the fly to the next instantiation
     (128, 7, 12), (128, 2, 12), (128, 1, 6), (64, 16, 6), (64, 13, 6), (128, 12, 12), (64, 9, 5), (128, 7, 10),
     (64, 19, 6), (256, 6, 25), (128, 3, 5), (128, 7, 13), (64, 8, 9),
+    # n % rows-per-step != 0: the last rows run one at a time after the last full step
+    (127, 6, 12), (129, 5, 10), (131, 8, 13), (63, 20, 6), (101, 3, 7), (126, 6, 12), (9, 4, 4), (65, 12, 6),
 ]
 
 

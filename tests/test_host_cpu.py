@@ -272,13 +272,13 @@ def test_dtw_kernel_choice_by_shape():
     assert name(256, 5, 51) == four  # C1b: compiled bucket
     for w in (4, 10, 11, 16, 25):  # run-time band, even and odd W
         assert name(128, 6, w) == four, w
-    assert name(126, 6, 12) == two  # n % 4 != 0
+    assert name(126, 6, 12) == four and name(127, 6, 12) == four  # n % 4 != 0: tail rows
+    assert name(63, 20, 6) == two and name(3, 6, 12) not in (four, two)  # n >= 2 x rows per step
     for d in (1, 2, 7):  # padded to 3 / 3 / 8 dimensions
         assert name(128, d, 12) == four, d
     for d in (9, 12, 13, 16, 19):  # padded to 12 / 16 / 20 dimensions at 2 rows per step
         assert name(128, d, 12) == two, d
     assert name(128, 6, 3) == two and name(128, 6, 1) not in (four, two)  # W >= rows per step
-    assert name(127, 6, 12) not in (four, two)  # odd n
     assert name(128, 24, 12) not in (four, two)  # d > 20
     assert name(1024, 8, 102) not in (four, two)  # C3's band row does not fit three blocks per SM
     assert name(128, 6, 12, dtype=1) not in (four, two)  # float64 without the filter: exact kernels
