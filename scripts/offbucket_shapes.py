@@ -6,6 +6,7 @@ dispatcher serves with another kernel.  Prints one line per shape: kernel,
 q/s, DTW ms, GCUPS and the fraction of the nominal FP32 issue peak.
 
     python scripts/offbucket_shapes.py > gpurun_out/offbucket.txt
+    python scripts/offbucket_shapes.py 128 6 10     # one shape
 """
 import sys
 from pathlib import Path
@@ -26,7 +27,10 @@ SHAPES = [  # (n, d, W)
 
 def main():
     nominal = 148 * 128 * 1.965e9
-    for n, d, w in SHAPES:
+    shapes = SHAPES
+    if len(sys.argv) == 4:  # one shape: n d W (for an ncu capture)
+        shapes = [tuple(int(v) for v in sys.argv[1:4])]
+    for n, d, w in shapes:
         spec = datasets.ConfigSpec(f"X{n}_{d}", 200000, 256, n, d, "f32", (w / n,), "sines", 50)
         rng = np.random.default_rng(0)
         vals = np.ascontiguousarray(datasets._sines_chunked(spec, spec.n_candidates + spec.n_queries, rng))
