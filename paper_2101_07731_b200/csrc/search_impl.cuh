@@ -2037,7 +2037,7 @@ __global__ void __launch_bounds__(64, MINB) dtw_laner_kernel(SArgs<float> a, Til
             } else {
                 pu = ps[j0 * R * 32];
             }
-            if constexpr (D <= 8) {
+            if constexpr (D <= 8 || MINB <= 5) {
                 // the first column of a block is read one block ahead (its
                 // consumer was the step's largest stall site: 9% of the samples)
                 float xn[2 * DP];
