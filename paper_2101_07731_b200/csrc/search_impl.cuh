@@ -2246,7 +2246,7 @@ static int launch_laner(const SArgs<float>& a, int d, int B, Tiles tl, int64_t n
 #define TCDTW_LANER_CASE(DD, BB, RR)                                                          \
     if (!pk.rt && pk.dims == DD && B == BB && pk.rows == RR) {                                \
         const int ww = LaneRLayout<DD, RR>::warp_words(a.n, a.qpad_rows, BB);                 \
-        return go(dtw_laner_kernel<DD, BB, RR, true, (DD >= 12 ? 5 : TCDTW_LANER_MINB)>, ww);                  \
+        return go(dtw_laner_kernel<DD, BB, RR, true, (DD >= 12 ? 5 : (BB >= 64 ? 3 : TCDTW_LANER_MINB))>, ww);                  \
     }
     TCDTW_LANER_SPECS(TCDTW_LANER_CASE)
 #undef TCDTW_LANER_CASE
